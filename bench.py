@@ -1,0 +1,396 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 GK bidiagonalization path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+One bench "step" is one call of the reference entry point on the
+configuration (default: config 2, `estimate_rank` of a 20000 x 5000 f64
+matrix with eps = 1e-6 relative, BASELINE.json configs[1]).  Metric: GK
+steps/s (k' GK iterations per call / time per call); the JSON line also
+carries time-to-result, effective HBM GB/s (2 m n bytes k' / time), the
+roofline of the A-streaming kernels, the CPU baseline and the end-to-end
+number through the public API with host buffers.
+
+  value : device-resident A (uploaded once), CUDA events on the library
+          stream around exactly K calls, barrier + sync on both sides,
+          max over ranks.  A (800 MB) is larger than L2 (126 MB), so every
+          pass streams HBM; no explicit flush needed.
+  e2e   : `estimate_rank(A_host)` with A in pinned host memory: upload of
+          this rank's rows + the run + the result read-back, per step.
+  roofline : per-launch CUDA-event durations of the gemv_n / gemv_t
+          kernels measured in a profiled repeat of the same K calls;
+          algorithmic bytes per launch = m_local * n * 8.
+  --impl reference : the CPU oracle port of the reference algorithm
+          (oracle/krylov_oracle.py, numpy/OpenBLAS on all host cores) on the
+          same matrix; each step is a bounded sample: 48 GK iterations.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = ("GK steps/s & time to top-k SVD; A·v+Aᵀu HBM GB/s vs roofline "
+          "at 1/2/4/8 GPU")
+UNIT = "GK steps/s"
+FALLBACK_HBM_GBS = 6650.0
+REF_SAMPLE_STEPS = 48
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload(cfg_id):
+    from paper_2104_10785_b200 import synth
+
+    if cfg_id == 1:
+        return dict(name="config1: fsvd k=30 r=10 eps=1e-10 of 2000x1000 f64 "
+                    "(U diag(10^(-4(i-1)/999)) V^T, seed 0)",
+                    m=2000, n=1000, make=lambda: synth.config1_matrix(seed=0),
+                    kind="fsvd", k=30, r=10, eps=1e-10, seed=0)
+    return dict(name="config2: estimate_rank eps=1e-6 relative of 20000x5000 f64 "
+                "(X Y^T + E, rank 137, seed 1)",
+                m=20000, n=5000, make=None, kind="rank", eps=1e-6, mode="relative", seed=1)
+
+
+def make_matrix(W, out=None):
+    from paper_2104_10785_b200 import synth
+
+    if W["kind"] == "fsvd":
+        A = W["make"]()
+        if out is not None:
+            out[...] = A
+            return out
+        return A
+    return synth.config2_matrix(seed=W["seed"], out=out)
+
+
+def call(K, W, A):
+    """One bench step through the public API; returns GK iterations done."""
+    if W["kind"] == "fsvd":
+        psvd = K.fsvd(A, k=W["k"], r=W["r"],
+                      cfg=K.BidiagConfig(k_max=W["k"], eps=W["eps"], seed=W["seed"]))
+        return W["k"], psvd.sigma.nbytes + psvd.U.nbytes + psvd.V.nbytes
+    rep = K.estimate_rank(A, eps=W["eps"], mode=W["mode"], cfg=K.BidiagConfig(k_max=1, seed=W["seed"]))
+    return rep.k_prime, 8 * (2 * rep.k_prime + 1)
+
+
+class ClockSampler:
+    """SM clocks and throttle reasons sampled during the timed region."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+        "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+        "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, device):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in self.REASONS.items():
+                    if mask & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_rank_sample(A, W, k_max):
+    """Oracle GK loop truncated at k_max steps: (gk steps, seconds)."""
+    from oracle import krylov_oracle as O
+
+    t0 = time.perf_counter()
+    g = O.gk_oracle(A, k_max, eps=1e-8, seed=W["seed"])
+    return g.k_prime, time.perf_counter() - t0
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        info = threadpool_info()
+        return max((i.get("num_threads", 1) for i in info), default=host_cores())
+    except Exception:  # noqa: BLE001
+        return host_cores()
+
+
+def peak_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy)"
+    except Exception:  # noqa: BLE001
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def traffic_from_profiles(cfg_id):
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        return json.loads(p.read_text()).get(f"config{cfg_id}")
+    except Exception:  # noqa: BLE001
+        return None
+
+
+# --------------------------------------------------------------------------- arms
+def run_reference(args, rank, world):
+    """Reference arm: the oracle port of the reference on the host CPU."""
+    if rank != 0:
+        return
+    W = workload(args.config)
+    A = make_matrix(W)
+    steps = []
+    for i in range(args.warmup + args.steps):
+        if W["kind"] == "fsvd":
+            from oracle import krylov_oracle as O
+
+            t0 = time.perf_counter()
+            O.fsvd_oracle(A, W["k"], W["r"], eps=W["eps"], seed=W["seed"])
+            kp, dt = W["k"], time.perf_counter() - t0
+        else:
+            kp, dt = cpu_rank_sample(A, W, REF_SAMPLE_STEPS)
+        if i >= args.warmup:
+            steps.append((kp, dt))
+    tot_k = sum(k for k, _ in steps)
+    tot_t = sum(t for _, t in steps)
+    val = tot_k / tot_t
+    cores = blas_threads()
+    sample = (f"{REF_SAMPLE_STEPS} GK iterations (k_max={REF_SAMPLE_STEPS}) of the config "
+              "matrix per step" if W["kind"] == "rank" else "one full fsvd call per step")
+    line = {
+        "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / len(steps),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": W["name"], "m": W["m"], "n": W["n"], "parallelism": "host cpu"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "effective_GBps": 2.0 * W["m"] * W["n"] * 8 * val / 1e9,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, dist):
+    import paper_2104_10785_b200 as K
+    from paper_2104_10785_b200 import _lib
+    from paper_2104_10785_b200.dist import init_distributed
+
+    ctx = init_distributed() if world > 1 else _lib.get_context()
+    W = workload(args.config)
+    m, n = W["m"], W["n"]
+
+    def barrier():
+        ctx.sync()
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    A = make_matrix(W)
+    op = K.DeviceMatrix.from_host(A)
+    m_local = op.m_local
+
+    # ---- value: device-resident A ----
+    for _ in range(args.warmup):
+        call(K, W, op)
+    barrier()
+    ctx.reset_stats()
+    kps = []
+    with ClockSampler(ctx.device) as clk:
+        ctx.mark(0)
+        for _ in range(args.steps):
+            kp, _ = call(K, W, op)
+            kps.append(kp)
+        ctx.mark(1)
+        barrier()
+    ms = max_over_ranks(ctx.elapsed_ms(0, 1))
+    launches = ctx.launch_count()
+    gk_steps = sum(kps)
+    value = gk_steps / (ms / 1e3)
+    eff_gbps = 2.0 * m * n * 8 * gk_steps / (ms / 1e3) / 1e9
+
+    # ---- roofline: profiled repeat of the same K calls ----
+    barrier()
+    ctx.reset_stats()
+    ctx.set_profiling(True)
+    for _ in range(args.steps):
+        call(K, W, op)
+    ctx.set_profiling(False)
+    stats = {c: ctx.kernel_stats(c) for c in range(5)}
+    barrier()
+    bytes_launch = float(m_local) * n * 8
+    nn, msn = stats[0]
+    nt, mst = stats[1]
+    peak, peak_src = peak_hbm()
+    per_kernel = {}
+    for name, (cnt, kms) in (("gemv_n", stats[0]), ("gemv_t", stats[1])):
+        if cnt:
+            per_kernel[name] = {"launches": cnt, "avg_us": 1e3 * kms / cnt,
+                                "GBps": bytes_launch / (kms / cnt / 1e3) / 1e9}
+    achieved = (bytes_launch * (nn + nt)) / ((msn + mst) / 1e3) / 1e9 if nn + nt else 0.0
+    tot_prof = sum(v[1] for v in stats.values())
+    roofline = {
+        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "frac": achieved / peak, "traffic": traffic_from_profiles(args.config),
+        "kernel": "gemv_n + gemv_t (A-streaming passes)", "peak_source": peak_src,
+        "bytes_per_launch": bytes_launch, "per_kernel": per_kernel,
+        "share_of_device_time": {k: v[1] / tot_prof for k, v in
+                                 zip(["gemv_n", "gemv_t", "cgs", "other", "finalize"],
+                                     stats.values())} if tot_prof else None,
+        "frac_of_nominal_8TBps": achieved / 8000.0,
+    }
+
+    # ---- e2e: public API with host (pinned) buffers ----
+    e2e = None
+    if not args.no_e2e:
+        import torch
+
+        pinned = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
+        A_host = pinned.numpy()
+        A_host[...] = A
+        for _ in range(min(args.warmup, 1)):
+            call(K, W, A_host)
+        barrier()
+        t_e2e = []
+        kps_e2e = []
+        d2h = 0
+        for _ in range(args.steps):
+            ctx.mark(2)
+            kp, nb = call(K, W, A_host)
+            ctx.mark(3)
+            ctx.sync()
+            t_e2e.append(ctx.elapsed_ms(2, 3))
+            kps_e2e.append(kp)
+            d2h = nb
+        barrier()
+        e_ms = max_over_ranks(sum(t_e2e))
+        e2e = {"value": sum(kps_e2e) / (e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(m_local * n * 8 + m_local * 8),
+               "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": e_ms / args.steps}
+        del pinned
+
+    # ---- CPU baseline (rank 0, N=1) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        if W["kind"] == "rank":
+            kp, dt = cpu_rank_sample(A, W, REF_SAMPLE_STEPS)
+            sample = f"oracle GK loop truncated at {REF_SAMPLE_STEPS} iterations on the config matrix"
+        else:
+            from oracle import krylov_oracle as O
+
+            t0 = time.perf_counter()
+            O.fsvd_oracle(A, W["k"], W["r"], eps=W["eps"], seed=W["seed"])
+            kp, dt = W["k"], time.perf_counter() - t0
+            sample = "one full oracle fsvd call"
+        cpu = {"value": kp / dt, "unit": UNIT, "cores": blas_threads(), "kind": "port",
+               "sample": sample, "seconds": dt}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": W["name"], "m": m, "n": n,
+                       "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+                       "l2": "A (%.0f MB) > L2 (126 MB): every pass streams HBM"
+                             % (m * n * 8 / 1e6)},
+            "time_to_result_s": ms / args.steps / 1e3,
+            "gk_steps_per_call": kps[0] if kps else None,
+            "effective_GBps": eff_gbps,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, dist)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,1011 @@
+// ksvd.cu -- C ABI (include/ksvd.h) over the sm_100a kernels in kernels.cuh.
+//
+// One context per GPU / process.  The GK loop (bidiag.py:111-184) is driven
+// from here: the host enqueues whole steps on the context stream, keeps all
+// scalars (alpha, beta) and the halting status on the device, and only
+// waits on the status of step i-kLag before enqueueing step i, so the GPU
+// never idles on a host round trip.  The stop rule depends only on device
+// status words that are identical on every rank, so all ranks issue the
+// same NCCL collectives in the same order.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "ksvd.h"
+
+using namespace ksvd;
+
+// ---------------------------------------------------------------------------
+// errors
+static thread_local std::string g_err;
+
+static int set_err(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(x)                                                                  \
+  do {                                                                         \
+    cudaError_t e_ = (x);                                                      \
+    if (e_ != cudaSuccess)                                                     \
+      return set_err(KSVD_ERUNTIME, "%s failed: %s (%s:%d)", #x,              \
+                     cudaGetErrorString(e_), __FILE__, __LINE__);              \
+  } while (0)
+#define NK(x)                                                                  \
+  do {                                                                         \
+    ncclResult_t r_ = (x);                                                     \
+    if (r_ != ncclSuccess)                                                     \
+      return set_err(KSVD_ERUNTIME, "%s failed: %s", #x,                      \
+                     ncclGetErrorString(r_));                                  \
+  } while (0)
+#define TRY(x)                                                                 \
+  do {                                                                         \
+    int rc_ = (x);                                                             \
+    if (rc_) return rc_;                                                       \
+  } while (0)
+
+int ksvd_set_error_from_host(int code, const char* msg) { return set_err(code, "%s", msg); }
+
+static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+static inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
+
+// ---------------------------------------------------------------------------
+// context
+enum KClass { KC_GEMV_N = 0, KC_GEMV_T = 1, KC_CGS = 2, KC_OTHER = 3, KC_FIN = 4, KC_NUM = 5 };
+
+struct ksvd_ctx {
+  int device = 0, rank = 0, nranks = 1, sms = 148;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  int64_t launches = 0;
+  bool profiling = false;
+  struct Prof {
+    cudaEvent_t a, b;
+    int cls;
+  };
+  std::vector<Prof> pending;
+  std::vector<cudaEvent_t> pool;
+  double prof_ms[KC_NUM] = {};
+  int64_t prof_n[KC_NUM] = {};
+  cudaEvent_t marks[8] = {};
+};
+
+static int get_event(ksvd_ctx* c, cudaEvent_t* ev) {
+  if (!c->pool.empty()) {
+    *ev = c->pool.back();
+    c->pool.pop_back();
+    return 0;
+  }
+  CK(cudaEventCreate(ev));
+  return 0;
+}
+
+static int collect_profile(ksvd_ctx* c) {
+  if (c->pending.empty()) return 0;
+  CK(cudaStreamSynchronize(c->stream));
+  for (auto& p : c->pending) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, p.a, p.b));
+    c->prof_ms[p.cls] += ms;
+    c->prof_n[p.cls] += 1;
+    c->pool.push_back(p.a);
+    c->pool.push_back(p.b);
+  }
+  c->pending.clear();
+  return 0;
+}
+
+template <typename Kern, typename... Args>
+static int launch(ksvd_ctx* c, int cls, Kern kernel, dim3 grid, dim3 block,
+                  size_t smem, Args... args) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (c->profiling) {
+    TRY(get_event(c, &a));
+    TRY(get_event(c, &b));
+    CK(cudaEventRecord(a, c->stream));
+  }
+  kernel<<<grid, block, smem, c->stream>>>(args...);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    return set_err(KSVD_ERUNTIME, "kernel launch failed: %s", cudaGetErrorString(e));
+  if (c->profiling) {
+    CK(cudaEventRecord(b, c->stream));
+    c->pending.push_back({a, b, cls});
+  }
+  c->launches++;
+  return 0;
+}
+
+static int allreduce(ksvd_ctx* c, double* buf, size_t count) {
+  if (c->nranks <= 1 || count == 0) return 0;
+  NK(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, c->comm, c->stream));
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// matrices
+struct GemvNPlan {
+  int V, nchunks, chunk_vecs, blocks_per_chunk;
+  int64_t nvec, groups_per_warp;
+  size_t smem;
+};
+struct GemvTPlan {
+  int64_t ncoltiles, nsplit, rows_per_split;
+};
+
+constexpr int kRowsPerWarp = 2;  // R of k_gemv_n
+constexpr int kUnrollN = 4;      // U of k_gemv_n
+constexpr int kUnrollT = 8;      // U of k_gemv_t
+constexpr int kMaxChunkDoubles = 8192;  // 64 KB of p per CTA
+
+struct ksvd_mat {
+  ksvd_ctx* ctx = nullptr;
+  int64_t m = 0, n = 0, row0 = 0, mloc = 0, lda = 0;
+  int64_t n_pad = 0, m_pad = 0;  // vector lengths (512 B multiples)
+  int dtype = KSVD_F64;
+  void* A = nullptr;
+  GemvNPlan pn{};
+  GemvTPlan pt{};
+  double* part_n = nullptr;  // nchunks x mloc  (nchunks > 1)
+  double* part_t = nullptr;  // nsplit x n_pad
+  // plain-product scratch
+  double *dx = nullptr, *dy = nullptr;
+  DevState* st0 = nullptr;  // always-running state for plain products
+};
+
+static size_t esize(int dtype) { return dtype == KSVD_F32 ? 4 : 8; }
+
+template <typename TA>
+static int set_smem_attr(size_t smem) {
+  auto kn = k_gemv_n<TA, kRowsPerWarp, kUnrollN>;
+  CK(cudaFuncSetAttribute(kn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  return 0;
+}
+
+template <typename TA>
+static int occupancy_n(size_t smem, int* out) {
+  auto kn = k_gemv_n<TA, kRowsPerWarp, kUnrollN>;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, kn, kThreads, smem));
+  return 0;
+}
+
+static int plan_matrix(ksvd_mat* M) {
+  ksvd_ctx* c = M->ctx;
+  const int64_t bytes = esize(M->dtype);
+  GemvNPlan& pn = M->pn;
+  pn.V = (int)(16 / bytes);
+  pn.nvec = cdiv(M->n, pn.V);
+  pn.nchunks = (int)cdiv(pn.nvec * pn.V, kMaxChunkDoubles);
+  pn.chunk_vecs = (int)cdiv(pn.nvec, pn.nchunks);
+  pn.smem = (size_t)pn.chunk_vecs * pn.V * sizeof(double);
+  int occ = 1;
+  if (M->dtype == KSVD_F32) {
+    TRY(set_smem_attr<float>(pn.smem));
+    TRY(occupancy_n<float>(pn.smem, &occ));
+  } else {
+    TRY(set_smem_attr<double>(pn.smem));
+    TRY(occupancy_n<double>(pn.smem, &occ));
+  }
+  occ = std::max(occ, 1);
+  const int64_t ngroups = cdiv(std::max<int64_t>(M->mloc, 1), kRowsPerWarp);
+  const int64_t warps_per_chunk =
+      std::max<int64_t>(1, (int64_t)c->sms * occ * kWarps / pn.nchunks);
+  pn.groups_per_warp = cdiv(ngroups, warps_per_chunk);
+  const int64_t warps_needed = cdiv(ngroups, pn.groups_per_warp);
+  pn.blocks_per_chunk = (int)cdiv(warps_needed, kWarps);
+
+  GemvTPlan& pt = M->pt;
+  pt.ncoltiles = cdiv(pn.nvec, kThreads);
+  const int64_t target = (int64_t)c->sms * 8;
+  int64_t nsplit = std::max<int64_t>(1, cdiv(target, pt.ncoltiles));
+  int64_t rps = std::max<int64_t>(64, cdiv(std::max<int64_t>(M->mloc, 1), nsplit));
+  pt.rows_per_split = rps;
+  pt.nsplit = std::max<int64_t>(1, cdiv(M->mloc, rps));
+  return 0;
+}
+
+static int alloc_matrix_buffers(ksvd_mat* M) {
+  const size_t abytes = (size_t)M->mloc * M->lda * esize(M->dtype);
+  CK(cudaMalloc(&M->A, std::max<size_t>(abytes, 16)));
+  TRY(plan_matrix(M));
+  if (M->pn.nchunks > 1)
+    CK(cudaMalloc(&M->part_n, sizeof(double) * M->pn.nchunks * std::max<int64_t>(M->mloc, 1)));
+  CK(cudaMalloc(&M->part_t, sizeof(double) * M->pt.nsplit * M->n_pad));
+  CK(cudaMalloc(&M->dx, sizeof(double) * std::max(M->n_pad, M->m_pad)));
+  CK(cudaMalloc(&M->dy, sizeof(double) * std::max(M->n_pad, M->m_pad)));
+  CK(cudaMemset(M->dx, 0, sizeof(double) * std::max(M->n_pad, M->m_pad)));
+  CK(cudaMemset(M->dy, 0, sizeof(double) * std::max(M->n_pad, M->m_pad)));
+  CK(cudaMalloc(&M->st0, sizeof(DevState)));
+  CK(cudaMemset(M->st0, 0, sizeof(DevState)));
+  return 0;
+}
+
+static int free_matrix(ksvd_mat* M) {
+  if (!M) return 0;
+  cudaSetDevice(M->ctx->device);
+  cudaStreamSynchronize(M->ctx->stream);
+  cudaFree(M->A);
+  cudaFree(M->part_n);
+  cudaFree(M->part_t);
+  cudaFree(M->dx);
+  cudaFree(M->dy);
+  cudaFree(M->st0);
+  delete M;
+  return 0;
+}
+
+// w = A p (- alpha q): p_src/p_scale/p_dst per k_gemv_n; out = w (m rows)
+static int enqueue_gemv_n(ksvd_mat* M, const double* p_src, const double* p_scale,
+                          double* p_dst, const double* qprev, const double* alpha,
+                          double* w, DevState* st, int step) {
+  ksvd_ctx* c = M->ctx;
+  const GemvNPlan& pn = M->pn;
+  if (M->mloc == 0) return 0;
+  const bool direct = pn.nchunks == 1;
+  dim3 grid(pn.blocks_per_chunk, pn.nchunks);
+  double* out = direct ? w : M->part_n;
+  const int64_t out_ld = direct ? 0 : M->mloc;
+  if (M->dtype == KSVD_F32) {
+    TRY(launch(c, KC_GEMV_N, k_gemv_n<float, kRowsPerWarp, kUnrollN>, grid,
+               dim3(kThreads), pn.smem, (const float*)M->A, M->lda, M->mloc,
+               pn.nvec, pn.chunk_vecs, p_src, p_scale, p_dst, M->n, out, out_ld,
+               direct ? qprev : (const double*)nullptr,
+               direct ? alpha : (const double*)nullptr, st, step,
+               pn.groups_per_warp));
+  } else {
+    TRY(launch(c, KC_GEMV_N, k_gemv_n<double, kRowsPerWarp, kUnrollN>, grid,
+               dim3(kThreads), pn.smem, (const double*)M->A, M->lda, M->mloc,
+               pn.nvec, pn.chunk_vecs, p_src, p_scale, p_dst, M->n, out, out_ld,
+               direct ? qprev : (const double*)nullptr,
+               direct ? alpha : (const double*)nullptr, st, step,
+               pn.groups_per_warp));
+  }
+  if (!direct) {
+    TRY(launch(c, KC_FIN, k_gemv_n_finalize, dim3((unsigned)cdiv(M->mloc, kThreads)),
+               dim3(kThreads), 0, (const double*)M->part_n, M->mloc, pn.nchunks,
+               M->mloc, qprev, alpha, w, st, step));
+  }
+  return 0;
+}
+
+// z = sum_ranks A^T q (- beta p): q_src/q_scale/q_dst per k_gemv_t.
+static int enqueue_gemv_t(ksvd_mat* M, const double* q_src, const double* q_scale,
+                          double* q_dst, const double* beta, const double* pprev,
+                          double* z, DevState* st, int step, bool check) {
+  ksvd_ctx* c = M->ctx;
+  const GemvTPlan& pt = M->pt;
+  if (M->mloc > 0) {
+    dim3 grid((unsigned)pt.ncoltiles, (unsigned)pt.nsplit);
+    if (M->dtype == KSVD_F32) {
+      TRY(launch(c, KC_GEMV_T, k_gemv_t<float, kUnrollT>, grid, dim3(kThreads), 0,
+                 (const float*)M->A, M->lda, M->mloc, M->pn.nvec, pt.rows_per_split,
+                 q_src, q_scale, q_dst, M->part_t, M->n_pad, (const DevState*)st));
+    } else {
+      TRY(launch(c, KC_GEMV_T, k_gemv_t<double, kUnrollT>, grid, dim3(kThreads), 0,
+                 (const double*)M->A, M->lda, M->mloc, M->pn.nvec, pt.rows_per_split,
+                 q_src, q_scale, q_dst, M->part_t, M->n_pad, (const DevState*)st));
+    }
+  } else {
+    CK(cudaMemsetAsync(M->part_t, 0, sizeof(double) * M->n_pad, c->stream));
+  }
+  const int nsplit = M->mloc > 0 ? (int)pt.nsplit : 1;
+  const bool multi = c->nranks > 1;
+  TRY(launch(c, KC_FIN, k_gemv_t_finalize, dim3((unsigned)cdiv(M->n_pad, kThreads)),
+             dim3(kThreads), 0, (const double*)M->part_t, M->n_pad, nsplit, M->n,
+             M->n_pad, multi ? (const double*)nullptr : beta,
+             multi ? (const double*)nullptr : pprev, z, st, step,
+             (int)(check && !multi)));
+  if (multi) {
+    TRY(allreduce(c, z, (size_t)M->n_pad));
+    if (check || pprev)
+      TRY(launch(c, KC_FIN, k_axpy_check, dim3((unsigned)cdiv(M->n, kThreads)),
+                 dim3(kThreads), 0, z, beta, pprev, M->n, st, step));
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// CGS2 against a basis (bidiag.py:77-87, 154-156, 171-173)
+struct CgsWork {
+  double* part = nullptr;  // nrb x cap
+  double* c = nullptr;     // cap
+  double* red = nullptr;   // 2
+  int64_t part_elems = 0;
+  int cap = 0;
+};
+
+static int choose_E(const ksvd_ctx* c, int64_t L) {
+  if (L >= (int64_t)kThreads * 4 * c->sms * 2) return 4;
+  if (L >= (int64_t)kThreads * 2 * c->sms) return 2;
+  return 1;
+}
+
+static int ensure_cgs(CgsWork* w, int64_t nrb, int cols) {
+  const int64_t need = nrb * std::max(cols, 1);
+  if (need > w->part_elems) {
+    cudaFree(w->part);
+    CK(cudaMalloc(&w->part, sizeof(double) * need));
+    w->part_elems = need;
+  }
+  if (cols > w->cap || !w->c) {
+    cudaFree(w->c);
+    w->cap = std::max(cols, 64);
+    CK(cudaMalloc(&w->c, sizeof(double) * w->cap));
+  }
+  if (!w->red) CK(cudaMalloc(&w->red, sizeof(double) * 4));
+  return 0;
+}
+
+template <int E>
+static int cgs_impl(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int ncols,
+                    double* x, int64_t L, int passes, bool sharded, double eps,
+                    double* slot, DevState* st, int step, int code) {
+  const int64_t nrb = std::max<int64_t>(1, cdiv(L, (int64_t)kThreads * E));
+  TRY(ensure_cgs(W, nrb, ncols));
+  const bool multi = sharded && c->nranks > 1;
+  double* part = W->part;
+  const unsigned rgrid = (unsigned)cdiv(std::max(ncols, 1), kWarps);
+  if (ncols == 0) {
+    TRY(launch(c, KC_CGS, k_sumsq<E>, dim3((unsigned)nrb), dim3(kThreads), 0,
+               (const double*)x, L, part, (const DevState*)st));
+  } else {
+    TRY(launch(c, KC_CGS, k_cgs_dot<E>, dim3((unsigned)nrb, (unsigned)cdiv(ncols, kJ)),
+               dim3(kThreads), 0, B, ldb, ncols, (const double*)x, L, part, (int)nrb,
+               (const DevState*)st));
+    TRY(launch(c, KC_CGS, k_reduce_cols, dim3(rgrid), dim3(kThreads), 0,
+               (const double*)part, (int)nrb, ncols, W->c, (const DevState*)st));
+    if (multi) TRY(allreduce(c, W->c, ncols));
+    for (int pass = 1; pass <= passes; ++pass) {
+      const int mode = pass < passes ? 1 : 2;
+      TRY(launch(c, KC_CGS, k_cgs_update<E>, dim3((unsigned)nrb), dim3(kThreads), 0, B,
+                 ldb, ncols, (const double*)W->c, x, L, mode, part, (int)nrb,
+                 (const DevState*)st));
+      if (mode == 1) {
+        TRY(launch(c, KC_CGS, k_reduce_cols, dim3(rgrid), dim3(kThreads), 0,
+                   (const double*)part, (int)nrb, ncols, W->c, (const DevState*)st));
+        if (multi) TRY(allreduce(c, W->c, ncols));
+      }
+    }
+  }
+  if (multi) {
+    TRY(launch(c, KC_CGS, k_norm_prep, dim3(1), dim3(32), 0, (const double*)part,
+               (int)nrb, W->red, (const DevState*)st));
+    TRY(allreduce(c, W->red, 2));
+    TRY(launch(c, KC_CGS, k_norm_test, dim3(1), dim3(32), 0, (const double*)nullptr, 0,
+               (const double*)W->red, eps, slot, st, step, code));
+  } else {
+    TRY(launch(c, KC_CGS, k_norm_test, dim3(1), dim3(32), 0, (const double*)part,
+               (int)nrb, (const double*)nullptr, eps, slot, st, step, code));
+  }
+  return 0;
+}
+
+// x <- x orthogonalised `passes` times against B[:, :ncols]; *slot = ||x||;
+// ||x|| < eps sets status `code` at `step`.
+static int cgs(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int ncols,
+               double* x, int64_t L, int passes, bool sharded, double eps,
+               double* slot, DevState* st, int step, int code) {
+  switch (choose_E(c, L)) {
+    case 4:
+      return cgs_impl<4>(c, W, B, ldb, ncols, x, L, passes, sharded, eps, slot, st, step, code);
+    case 2:
+      return cgs_impl<2>(c, W, B, ldb, ncols, x, L, passes, sharded, eps, slot, st, step, code);
+    default:
+      return cgs_impl<1>(c, W, B, ldb, ncols, x, L, passes, sharded, eps, slot, st, step, code);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// runs
+constexpr int kLag = 3;   // steps enqueued ahead of the last checked status
+constexpr int kRing = 8;  // pinned status ring
+
+struct ksvd_run {
+  ksvd_mat* M = nullptr;
+  int k_max = 0, reorth = 2, cap = 0;
+  double eps = 1e-8;
+  double *Q = nullptr, *P = nullptr;  // column-major bases
+  int64_t ldq = 0, ldp = 0;
+  double *w = nullptr, *z = nullptr;
+  double *alpha = nullptr, *beta = nullptr;  // 1-based: alpha[i] = alpha_i
+  DevState* st = nullptr;
+  DevState* st_aux = nullptr;  // terminal column / Ritz filter
+  CgsWork left, right;
+  double* slot = nullptr;  // scratch scalars
+  int kprime = 0, flags = 0, status = 0;
+  // Ritz
+  double *G = nullptr, *V = nullptr, *U = nullptr, *sig = nullptr;
+  int* h_ring = nullptr;
+  cudaEvent_t ring_ev[kRing] = {};
+};
+
+static int grow_bases(ksvd_run* R, int need_cols) {
+  // Q needs need_cols+1 columns, P need_cols columns.
+  if (need_cols <= R->cap) return 0;
+  ksvd_ctx* c = R->M->ctx;
+  int ncap = std::max(need_cols, std::min(R->k_max, std::max(2 * R->cap, 64)));
+  ncap = std::min(ncap, R->k_max);
+  double *Qn = nullptr, *Pn = nullptr;
+  CK(cudaMallocAsync(&Qn, sizeof(double) * R->ldq * (ncap + 1), c->stream));
+  CK(cudaMallocAsync(&Pn, sizeof(double) * R->ldp * ncap, c->stream));
+  CK(cudaMemsetAsync(Qn, 0, sizeof(double) * R->ldq * (ncap + 1), c->stream));
+  CK(cudaMemsetAsync(Pn, 0, sizeof(double) * R->ldp * ncap, c->stream));
+  if (R->Q) {
+    CK(cudaMemcpyAsync(Qn, R->Q, sizeof(double) * R->ldq * (R->cap + 1),
+                       cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(Pn, R->P, sizeof(double) * R->ldp * R->cap,
+                       cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaFreeAsync(R->Q, c->stream));
+    CK(cudaFreeAsync(R->P, c->stream));
+  }
+  R->Q = Qn;
+  R->P = Pn;
+  R->cap = ncap;
+  return 0;
+}
+
+static void free_run(ksvd_run* R) {
+  if (!R) return;
+  ksvd_ctx* c = R->M->ctx;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (double* p : {R->Q, R->P, R->w, R->z, R->alpha, R->beta, R->slot, R->G, R->V,
+                    R->U, R->sig, R->left.part, R->left.c, R->left.red, R->right.part,
+                    R->right.c, R->right.red})
+    cudaFree(p);
+  cudaFree(R->st);
+  cudaFree(R->st_aux);
+  for (auto& e : R->ring_ev)
+    if (e) cudaEventDestroy(e);
+  if (R->h_ring) cudaFreeHost(R->h_ring);
+  delete R;
+}
+
+static double* Qcol(ksvd_run* R, int j) { return R->Q + (int64_t)j * R->ldq; }
+static double* Pcol(ksvd_run* R, int j) { return R->P + (int64_t)j * R->ldp; }
+
+// One GK iteration i (1-based), bidiag.py:151-178.
+static int enqueue_step(ksvd_run* R, int i) {
+  ksvd_mat* M = R->M;
+  ksvd_ctx* c = M->ctx;
+  TRY(grow_bases(R, i + 1 <= R->k_max ? i + 1 : i));
+  // w = A p_i - alpha_i q_i, with p_i = z / alpha_i stored to P[:, i-1]
+  TRY(enqueue_gemv_n(M, R->z, R->alpha + i, Pcol(R, i - 1), Qcol(R, i - 1), R->alpha + i,
+                     R->w, R->st, i));
+  // CGS2 against Q[:, :i]; beta_{i+1} = ||w||; beta < eps -> breakdown
+  TRY(cgs(c, &R->left, R->Q, R->ldq, i, R->w, M->mloc, R->reorth, true, R->eps,
+          R->beta + i + 1, R->st, i, ST_BETA_BREAK));
+  if (i == R->k_max) {
+    // q_{k+1} = w / beta; stop before alpha_{k+1} (bidiag.py:165-168)
+    TRY(launch(c, KC_OTHER, k_scale, dim3((unsigned)cdiv(std::max<int64_t>(M->mloc, 1), kThreads)),
+               dim3(kThreads), 0, (const double*)R->w, (const double*)(R->beta + i + 1),
+               Qcol(R, i), M->mloc, (const DevState*)R->st));
+    return 0;
+  }
+  // z = A^T q_{i+1} - beta_{i+1} p_i, q_{i+1} = w / beta stored to Q[:, i]
+  TRY(enqueue_gemv_t(M, R->w, R->beta + i + 1, Qcol(R, i), R->beta + i + 1, Pcol(R, i - 1),
+                     R->z, R->st, i, true));
+  // CGS2 against P[:, :i] (replicated, no collective); alpha_{i+1} = ||z||
+  TRY(cgs(c, &R->right, R->P, R->ldp, i, R->z, M->n, R->reorth, false, R->eps,
+          R->alpha + i + 1, R->st, i, ST_ALPHA_BREAK));
+  return 0;
+}
+
+static int read_state(ksvd_run* R) {
+  ksvd_ctx* c = R->M->ctx;
+  DevState h{};
+  CK(cudaMemcpyAsync(&h, R->st, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  R->status = h.status;
+  R->flags = 0;
+  switch (h.status) {
+    case ST_RUNNING:
+      R->kprime = R->k_max;
+      break;
+    case ST_DEGENERATE:
+      R->kprime = 0;
+      R->flags = KSVD_RUN_EARLY | KSVD_RUN_DEGENERATE;
+      break;
+    case ST_BETA_BREAK:
+      R->kprime = h.kprime;
+      R->flags = KSVD_RUN_EARLY | KSVD_RUN_BETA_BREAK;
+      break;
+    case ST_ALPHA_BREAK:
+      R->kprime = h.kprime;
+      R->flags = KSVD_RUN_EARLY | KSVD_RUN_ALPHA_BREAK;
+      break;
+    case ST_NONFINITE:
+    default:
+      R->kprime = h.kprime;
+      return set_err(KSVD_ENUMERIC, "non-finite values encountered in the GK step %d "
+                     "(A p_i or A^T q_i)", h.where);
+  }
+  return 0;
+}
+
+static int run_loop(ksvd_run* R, const double* q1_local) {
+  ksvd_mat* M = R->M;
+  ksvd_ctx* c = M->ctx;
+  TRY(grow_bases(R, std::min(R->k_max, 64)));
+  if (M->mloc > 0)
+    CK(cudaMemcpyAsync(R->Q, q1_local, sizeof(double) * M->mloc, cudaMemcpyHostToDevice,
+                       c->stream));
+  // z = A^T q_1; alpha_1 = ||z||; alpha_1 < eps -> degenerate (bidiag.py:139-145)
+  TRY(enqueue_gemv_t(M, R->Q, nullptr, nullptr, nullptr, nullptr, R->z, R->st, 0, true));
+  TRY(cgs(c, &R->right, R->P, R->ldp, 0, R->z, M->n, 0, false, R->eps, R->alpha + 1, R->st,
+          0, ST_DEGENERATE));
+  for (int i = 1; i <= R->k_max; ++i) {
+    if (i > kLag) {
+      const int s = (i - kLag) % kRing;
+      CK(cudaEventSynchronize(R->ring_ev[s]));
+      if (R->h_ring[s] != ST_RUNNING) break;
+    }
+    TRY(enqueue_step(R, i));
+    const int s = i % kRing;
+    CK(cudaMemcpyAsync(R->h_ring + s, &R->st->status, sizeof(int), cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaEventRecord(R->ring_ev[s], c->stream));
+  }
+  return read_state(R);
+}
+
+template <typename TA>
+static int enqueue_multi_rhs(ksvd_mat* M, const double* X, int64_t ldx, int k,
+                             const double* sigma, double* Y, int64_t ldy) {
+  if (M->mloc == 0 || k == 0) return 0;
+  dim3 grid((unsigned)cdiv(M->mloc, kMR), (unsigned)cdiv(k, 32));
+  return launch(M->ctx, KC_OTHER, k_multi_rhs<TA>, grid, dim3(kThreads), 0,
+                (const TA*)M->A, M->lda, M->mloc, M->n, X, ldx, k, sigma, Y, ldy);
+}
+
+static int multi_rhs(ksvd_mat* M, const double* X, int64_t ldx, int k, const double* sigma,
+                     double* Y, int64_t ldy) {
+  if (M->dtype == KSVD_F32) return enqueue_multi_rhs<float>(M, X, ldx, k, sigma, Y, ldy);
+  return enqueue_multi_rhs<double>(M, X, ldx, k, sigma, Y, ldy);
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+extern "C" {
+
+const char* ksvd_last_error(void) { return g_err.c_str(); }
+int ksvd_version(void) { return 1; }
+
+int ksvd_device_count(int* count) {
+  CK(cudaGetDeviceCount(count));
+  return 0;
+}
+
+int ksvd_nccl_unique_id(char* uid) {
+  ncclUniqueId id;
+  NK(ncclGetUniqueId(&id));
+  static_assert(sizeof(id) == KSVD_NCCL_UID_BYTES, "ncclUniqueId size");
+  memcpy(uid, &id, sizeof id);
+  return 0;
+}
+
+int ksvd_ctx_create(int device, int rank, int nranks, const char* uid, ksvd_ctx** out) {
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    return set_err(KSVD_ECONFIG, "bad rank %d / nranks %d", rank, nranks);
+  if (nranks > 1 && !uid) return set_err(KSVD_ECONFIG, "nranks > 1 needs a NCCL unique id");
+  CK(cudaSetDevice(device));
+  auto* c = new ksvd_ctx();
+  c->device = device;
+  c->rank = rank;
+  c->nranks = nranks;
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  c->sms = prop.multiProcessorCount;
+  CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  for (auto& e : c->marks) CK(cudaEventCreate(&e));
+  if (nranks > 1) {
+    ncclUniqueId id;
+    memcpy(&id, uid, sizeof id);
+    NK(ncclCommInitRank(&c->comm, nranks, id, rank));
+  }
+  *out = c;
+  return 0;
+}
+
+int ksvd_ctx_destroy(ksvd_ctx* c) {
+  if (!c) return 0;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  if (c->comm) ncclCommDestroy(c->comm);
+  for (auto& p : c->pending) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : c->pool) cudaEventDestroy(e);
+  for (auto e : c->marks) cudaEventDestroy(e);
+  cudaStreamDestroy(c->stream);
+  delete c;
+  return 0;
+}
+
+int ksvd_ctx_sync(ksvd_ctx* c) {
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int ksvd_ctx_set_profiling(ksvd_ctx* c, int on) {
+  TRY(collect_profile(c));
+  c->profiling = on != 0;
+  return 0;
+}
+
+int ksvd_ctx_kernel_stats(ksvd_ctx* c, int cls, int64_t* launches, double* ms) {
+  if (cls < 0 || cls >= KC_NUM) return set_err(KSVD_ECONFIG, "kernel class %d", cls);
+  CK(cudaSetDevice(c->device));
+  TRY(collect_profile(c));
+  *launches = c->prof_n[cls];
+  *ms = c->prof_ms[cls];
+  return 0;
+}
+
+int ksvd_ctx_reset_stats(ksvd_ctx* c) {
+  CK(cudaSetDevice(c->device));
+  TRY(collect_profile(c));
+  for (int i = 0; i < KC_NUM; ++i) {
+    c->prof_ms[i] = 0;
+    c->prof_n[i] = 0;
+  }
+  c->launches = 0;
+  return 0;
+}
+
+int ksvd_ctx_launch_count(ksvd_ctx* c, int64_t* launches) {
+  *launches = c->launches;
+  return 0;
+}
+
+int ksvd_ctx_mark(ksvd_ctx* c, int slot) {
+  if (slot < 0 || slot >= 8) return set_err(KSVD_ECONFIG, "mark slot %d", slot);
+  CK(cudaSetDevice(c->device));
+  CK(cudaEventRecord(c->marks[slot], c->stream));
+  return 0;
+}
+
+int ksvd_ctx_elapsed(ksvd_ctx* c, int s0, int s1, float* ms) {
+  if (s0 < 0 || s0 >= 8 || s1 < 0 || s1 >= 8) return set_err(KSVD_ECONFIG, "mark slot");
+  CK(cudaSetDevice(c->device));
+  CK(cudaEventSynchronize(c->marks[s1]));
+  CK(cudaEventElapsedTime(ms, c->marks[s0], c->marks[s1]));
+  return 0;
+}
+
+static int matrix_new(ksvd_ctx* c, const void* rows, int64_t m, int64_t n, int64_t row0,
+                      int64_t mloc, int64_t src_ld, int dtype, cudaMemcpyKind kind,
+                      ksvd_mat** out) {
+  if (m < 1 || n < 1)
+    return set_err(KSVD_ECONFIG, "expected a non-empty 2-d matrix, got %lldx%lld",
+                   (long long)m, (long long)n);
+  if (dtype != KSVD_F64 && dtype != KSVD_F32) return set_err(KSVD_ECONFIG, "dtype %d", dtype);
+  if (row0 < 0 || mloc < 0 || row0 + mloc > m)
+    return set_err(KSVD_ECONFIG, "row shard [%lld, %lld) outside %lld rows",
+                   (long long)row0, (long long)(row0 + mloc), (long long)m);
+  if (src_ld < n) return set_err(KSVD_ECONFIG, "src_ld %lld < n %lld", (long long)src_ld,
+                                 (long long)n);
+  CK(cudaSetDevice(c->device));
+  auto* M = new ksvd_mat();
+  M->ctx = c;
+  M->m = m;
+  M->n = n;
+  M->row0 = row0;
+  M->mloc = mloc;
+  M->dtype = dtype;
+  const int64_t es = (int64_t)esize(dtype);
+  M->lda = rup(n, 512 / es);
+  M->n_pad = rup(n, 64);
+  M->m_pad = rup(std::max<int64_t>(mloc, 1), 64);
+  int rc = alloc_matrix_buffers(M);
+  if (rc) {
+    free_matrix(M);
+    return rc;
+  }
+  if (mloc > 0) {
+    if (M->lda > n) {
+      cudaError_t e = cudaMemsetAsync(M->A, 0, (size_t)mloc * M->lda * es, c->stream);
+      if (e != cudaSuccess) {
+        free_matrix(M);
+        return set_err(KSVD_ERUNTIME, "memset: %s", cudaGetErrorString(e));
+      }
+    }
+    cudaError_t e = cudaMemcpy2DAsync(M->A, (size_t)M->lda * es, rows, (size_t)src_ld * es,
+                                      (size_t)n * es, (size_t)mloc, kind, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+      free_matrix(M);
+      return set_err(KSVD_ERUNTIME, "matrix upload: %s", cudaGetErrorString(e));
+    }
+  }
+  *out = M;
+  return 0;
+}
+
+int ksvd_matrix_from_host(ksvd_ctx* c, const void* rows, int64_t m, int64_t n, int64_t row0,
+                          int64_t mloc, int64_t src_ld, int dtype, ksvd_mat** out) {
+  return matrix_new(c, rows, m, n, row0, mloc, src_ld, dtype, cudaMemcpyHostToDevice, out);
+}
+
+int ksvd_matrix_from_device(ksvd_ctx* c, const void* rows, int64_t m, int64_t n,
+                            int64_t row0, int64_t mloc, int64_t src_ld, int dtype,
+                            ksvd_mat** out) {
+  return matrix_new(c, rows, m, n, row0, mloc, src_ld, dtype, cudaMemcpyDeviceToDevice, out);
+}
+
+int ksvd_matrix_free(ksvd_mat* M) { return free_matrix(M); }
+
+int ksvd_matrix_shape(ksvd_mat* M, int64_t* m, int64_t* n, int64_t* row0, int64_t* mloc,
+                      int* dtype, int64_t* ld) {
+  if (m) *m = M->m;
+  if (n) *n = M->n;
+  if (row0) *row0 = M->row0;
+  if (mloc) *mloc = M->mloc;
+  if (dtype) *dtype = M->dtype;
+  if (ld) *ld = M->lda;
+  return 0;
+}
+
+int ksvd_matrix_to_host(ksvd_mat* M, void* rows) {
+  ksvd_ctx* c = M->ctx;
+  CK(cudaSetDevice(c->device));
+  if (M->mloc == 0) return 0;
+  const size_t es = esize(M->dtype);
+  CK(cudaMemcpy2DAsync(rows, (size_t)M->n * es, M->A, (size_t)M->lda * es, (size_t)M->n * es,
+                       (size_t)M->mloc, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+static int reset_state(ksvd_ctx* c, DevState* st) {
+  CK(cudaMemsetAsync(st, 0, sizeof(DevState), c->stream));
+  return 0;
+}
+
+int ksvd_matvec(ksvd_mat* M, const double* x, double* y) {
+  ksvd_ctx* c = M->ctx;
+  CK(cudaSetDevice(c->device));
+  TRY(reset_state(c, M->st0));
+  CK(cudaMemcpyAsync(M->dx, x, sizeof(double) * M->n, cudaMemcpyHostToDevice, c->stream));
+  TRY(enqueue_gemv_n(M, M->dx, nullptr, nullptr, nullptr, nullptr, M->dy, M->st0, 0));
+  if (M->mloc > 0)
+    CK(cudaMemcpyAsync(y, M->dy, sizeof(double) * M->mloc, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int ksvd_rmatvec(ksvd_mat* M, const double* y, double* z) {
+  ksvd_ctx* c = M->ctx;
+  CK(cudaSetDevice(c->device));
+  TRY(reset_state(c, M->st0));
+  if (M->mloc > 0)
+    CK(cudaMemcpyAsync(M->dx, y, sizeof(double) * M->mloc, cudaMemcpyHostToDevice, c->stream));
+  TRY(enqueue_gemv_t(M, M->dx, nullptr, nullptr, nullptr, nullptr, M->dy, M->st0, 0, false));
+  CK(cudaMemcpyAsync(z, M->dy, sizeof(double) * M->n, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int ksvd_matmat(ksvd_mat* M, const double* X, int k, double* Y) {
+  ksvd_ctx* c = M->ctx;
+  CK(cudaSetDevice(c->device));
+  if (k <= 0) return k == 0 ? 0 : set_err(KSVD_ECONFIG, "k = %d", k);
+  double *dX = nullptr, *dY = nullptr;
+  CK(cudaMallocAsync(&dX, sizeof(double) * M->n * k, c->stream));
+  CK(cudaMallocAsync(&dY, sizeof(double) * std::max<int64_t>(M->mloc, 1) * k, c->stream));
+  CK(cudaMemcpyAsync(dX, X, sizeof(double) * M->n * k, cudaMemcpyHostToDevice, c->stream));
+  int rc = multi_rhs(M, dX, M->n, k, nullptr, dY, M->mloc);
+  if (!rc && M->mloc > 0) {
+    cudaError_t e = cudaMemcpyAsync(Y, dY, sizeof(double) * M->mloc * k,
+                                    cudaMemcpyDeviceToHost, c->stream);
+    if (e != cudaSuccess) rc = set_err(KSVD_ERUNTIME, "matmat D2H: %s", cudaGetErrorString(e));
+  }
+  cudaFreeAsync(dX, c->stream);
+  cudaFreeAsync(dY, c->stream);
+  CK(cudaStreamSynchronize(c->stream));
+  return rc;
+}
+
+int ksvd_gk_run(ksvd_mat* M, int k_max, double eps, int reorth, const double* q1_local,
+                ksvd_run** out) {
+  ksvd_ctx* c = M->ctx;
+  if (k_max < 1 || k_max > std::min(M->m, M->n))
+    return set_err(KSVD_ECONFIG, "k_max must be in [1, min(m,n)] = [1, %lld], got %d",
+                   (long long)std::min(M->m, M->n), k_max);
+  if (!(eps > 0)) return set_err(KSVD_ECONFIG, "eps must be > 0, got %g", eps);
+  if (reorth != 1 && reorth != 2)
+    return set_err(KSVD_ECONFIG, "reorth_passes must be 1 or 2, got %d", reorth);
+  CK(cudaSetDevice(c->device));
+  auto* R = new ksvd_run();
+  R->M = M;
+  R->k_max = k_max;
+  R->eps = eps;
+  R->reorth = reorth;
+  R->ldq = M->m_pad;
+  R->ldp = M->n_pad;
+  auto fail = [&](int rc) {
+    free_run(R);
+    return rc;
+  };
+  cudaError_t e = cudaSuccess;
+#define RUN_CK(x)                                                             \
+  do {                                                                        \
+    e = (x);                                                                  \
+    if (e != cudaSuccess)                                                     \
+      return fail(set_err(KSVD_ERUNTIME, "%s: %s", #x, cudaGetErrorString(e))); \
+  } while (0)
+  RUN_CK(cudaMalloc(&R->w, sizeof(double) * R->ldq));
+  RUN_CK(cudaMalloc(&R->z, sizeof(double) * R->ldp));
+  RUN_CK(cudaMemsetAsync(R->w, 0, sizeof(double) * R->ldq, c->stream));
+  RUN_CK(cudaMemsetAsync(R->z, 0, sizeof(double) * R->ldp, c->stream));
+  RUN_CK(cudaMalloc(&R->alpha, sizeof(double) * (k_max + 2)));
+  RUN_CK(cudaMalloc(&R->beta, sizeof(double) * (k_max + 3)));
+  RUN_CK(cudaMemsetAsync(R->alpha, 0, sizeof(double) * (k_max + 2), c->stream));
+  RUN_CK(cudaMemsetAsync(R->beta, 0, sizeof(double) * (k_max + 3), c->stream));
+  RUN_CK(cudaMalloc(&R->slot, sizeof(double) * 8));
+  RUN_CK(cudaMalloc(&R->st, sizeof(DevState)));
+  RUN_CK(cudaMalloc(&R->st_aux, sizeof(DevState)));
+  RUN_CK(cudaMemsetAsync(R->st, 0, sizeof(DevState), c->stream));
+  RUN_CK(cudaMemsetAsync(R->st_aux, 0, sizeof(DevState), c->stream));
+  RUN_CK(cudaMallocHost(&R->h_ring, sizeof(int) * kRing));
+  for (auto& ev : R->ring_ev) RUN_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+#undef RUN_CK
+  int rc = run_loop(R, q1_local);
+  if (rc) return fail(rc);
+  *out = R;
+  return 0;
+}
+
+int ksvd_run_info(ksvd_run* R, int* k_prime, int* flags, double* alphas, double* betas) {
+  ksvd_ctx* c = R->M->ctx;
+  CK(cudaSetDevice(c->device));
+  if (k_prime) *k_prime = R->kprime;
+  if (flags) *flags = R->flags;
+  const int kp = R->kprime;
+  if (alphas && kp > 0)
+    CK(cudaMemcpyAsync(alphas, R->alpha + 1, sizeof(double) * kp, cudaMemcpyDeviceToHost,
+                       c->stream));
+  // betas[1..k'] = beta_2..beta_{k'+1}
+  if (betas && kp > 0 && !(R->flags & KSVD_RUN_DEGENERATE))
+    CK(cudaMemcpyAsync(betas + 1, R->beta + 2, sizeof(double) * kp, cudaMemcpyDeviceToHost,
+                       c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int ksvd_run_extend(ksvd_run* R, const double* v_local, double nrm, int* accepted) {
+  ksvd_mat* M = R->M;
+  ksvd_ctx* c = M->ctx;
+  CK(cudaSetDevice(c->device));
+  const int kp = R->kprime;
+  if (kp >= M->m) return set_err(KSVD_ECONFIG, "left space exhausted (k' = m)");
+  TRY(grow_bases(R, std::min(kp, R->k_max)));
+  TRY(reset_state(c, R->st_aux));
+  if (v_local && M->mloc > 0)
+    CK(cudaMemcpyAsync(R->w, v_local, sizeof(double) * M->mloc, cudaMemcpyHostToDevice,
+                       c->stream));
+  const unsigned g = (unsigned)cdiv(std::max<int64_t>(M->mloc, 1), kThreads);
+  TRY(launch(c, KC_OTHER, k_scale_val, dim3(g), dim3(kThreads), 0, (const double*)R->w, nrm,
+             R->w, M->mloc, (const DevState*)R->st_aux));
+  // v = orthogonalize(v, Q[:, :k'], passes=2); nrm2 = ||v||  (bidiag.py:102-103)
+  TRY(cgs(c, &R->left, R->Q, R->ldq, kp, R->w, M->mloc, 2, true, 0.5, R->slot,
+          R->st_aux, kp, ST_CUT));
+  DevState h{};
+  CK(cudaMemcpyAsync(&h, R->st_aux, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+  double nrm2 = 0;
+  CK(cudaMemcpyAsync(&nrm2, R->slot, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (h.status == ST_NONFINITE)
+    return set_err(KSVD_ENUMERIC, "non-finite values in the terminal column");
+  // accepted iff nrm2 > 0.5 (strict): the CUT test above fires for < 0.5
+  *accepted = (h.status == ST_RUNNING && nrm2 > 0.5) ? 1 : 0;
+  if (*accepted) {
+    TRY(reset_state(c, R->st_aux));
+    TRY(launch(c, KC_OTHER, k_scale, dim3(g), dim3(kThreads), 0, (const double*)R->w,
+               (const double*)R->slot, Qcol(R, kp), M->mloc, (const DevState*)R->st_aux));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  return 0;
+}
+
+int ksvd_run_bases(ksvd_run* R, double* Q, int q_cols, double* P, int p_cols) {
+  ksvd_mat* M = R->M;
+  ksvd_ctx* c = M->ctx;
+  CK(cudaSetDevice(c->device));
+  if (q_cols < 0 || q_cols > R->cap + 1 || p_cols < 0 || p_cols > R->cap)
+    return set_err(KSVD_ECONFIG, "bases: %d/%d columns requested, %d allocated", q_cols,
+                   p_cols, R->cap);
+  if (Q && q_cols > 0 && M->mloc > 0)
+    CK(cudaMemcpy2DAsync(Q, sizeof(double) * M->mloc, R->Q, sizeof(double) * R->ldq,
+                         sizeof(double) * M->mloc, q_cols, cudaMemcpyDeviceToHost, c->stream));
+  if (P && p_cols > 0)
+    CK(cudaMemcpy2DAsync(P, sizeof(double) * M->n, R->P, sizeof(double) * R->ldp,
+                         sizeof(double) * M->n, p_cols, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int ksvd_ritz(ksvd_run* R, const double* G, const double* sigma, int take, int ortho,
+              double* U, double* V, int* n_good) {
+  ksvd_mat* M = R->M;
+  ksvd_ctx* c = M->ctx;
+  CK(cudaSetDevice(c->device));
+  const int kp = R->kprime;
+  if (take < 0 || take > kp) return set_err(KSVD_ECONFIG, "take %d outside [0, k'=%d]", take, kp);
+  *n_good = 0;
+  if (take == 0) return 0;
+  const int64_t ldu = M->m_pad, ldv = M->n_pad;
+  cudaFree(R->G);
+  cudaFree(R->V);
+  cudaFree(R->U);
+  cudaFree(R->sig);
+  R->G = R->V = R->U = R->sig = nullptr;
+  CK(cudaMalloc(&R->G, sizeof(double) * kp * take));
+  CK(cudaMalloc(&R->V, sizeof(double) * ldv * take));
+  CK(cudaMalloc(&R->U, sizeof(double) * ldu * take));
+  CK(cudaMalloc(&R->sig, sizeof(double) * take));
+  CK(cudaMemsetAsync(R->V, 0, sizeof(double) * ldv * take, c->stream));
+  CK(cudaMemsetAsync(R->U, 0, sizeof(double) * ldu * take, c->stream));
+  CK(cudaMemcpyAsync(R->G, G, sizeof(double) * kp * take, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(R->sig, sigma, sizeof(double) * take, cudaMemcpyHostToDevice, c->stream));
+  // V = P[:, :k'] G  (fsvd.py:191)
+  TRY(launch(c, KC_OTHER, k_basis_combine, dim3((unsigned)cdiv(M->n, kThreads), (unsigned)cdiv(take, kTT)),
+             dim3(kThreads), 0, (const double*)R->P, R->ldp, M->n, kp, (const double*)R->G, take,
+             R->V, ldv));
+  // U[:, t] = A V[:, t] / sigma_t, one pass over A (fsvd.py:192-194)
+  TRY(multi_rhs(M, R->V, ldv, take, R->sig, R->U, ldu));
+  int good = take;
+  if (ortho) {
+    // CGS2 column filter, cut at the first residual < 1e-2 (fsvd.py:145-155)
+    TRY(reset_state(c, R->st_aux));
+    const unsigned g = (unsigned)cdiv(std::max<int64_t>(M->mloc, 1), kThreads);
+    for (int t = 0; t < take; ++t) {
+      double* ut = R->U + (int64_t)t * ldu;
+      TRY(cgs(c, &R->left, R->U, ldu, t, ut, M->mloc, 2, true, 1e-2, R->slot + (t % 8),
+              R->st_aux, t, ST_CUT));
+      TRY(launch(c, KC_OTHER, k_scale, dim3(g), dim3(kThreads), 0, (const double*)ut,
+                 (const double*)(R->slot + (t % 8)), ut, M->mloc, (const DevState*)R->st_aux));
+    }
+    DevState h{};
+    CK(cudaMemcpyAsync(&h, R->st_aux, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (h.status == ST_NONFINITE) return set_err(KSVD_ENUMERIC, "non-finite Ritz vectors");
+    if (h.status == ST_CUT) good = h.kprime;
+  }
+  // fix_signs (linops.py:271-282)
+  if (good > 0)
+    TRY(launch(c, KC_OTHER, k_fix_signs, dim3(good), dim3(kThreads), 0, R->V, ldv, M->n, R->U,
+               ldu, M->mloc));
+  if (good > 0) {
+    if (M->mloc > 0)
+      CK(cudaMemcpy2DAsync(U, sizeof(double) * M->mloc, R->U, sizeof(double) * ldu,
+                           sizeof(double) * M->mloc, good, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpy2DAsync(V, sizeof(double) * M->n, R->V, sizeof(double) * ldv,
+                         sizeof(double) * M->n, good, cudaMemcpyDeviceToHost, c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  *n_good = good;
+  return 0;
+}
+
+int ksvd_run_free(ksvd_run* R) {
+  free_run(R);
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,80 @@
+"""The C-ABI library: loads, exports every symbol include/ksvd.h declares,
+and its host-side spectral stage matches the reference (CPU only; no
+compute call touches a GPU here)."""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2104_10785_b200 import _lib, symtridiag_eig, SymTridiag
+from paper_2104_10785_b200.build import LIB, needs_build
+from tests.parity import col_cos
+
+HEADER = Path(__file__).resolve().parent.parent / "include" / "ksvd.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"\b(ksvd_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_built_and_loads():
+    assert LIB.exists(), "run python -m paper_2104_10785_b200.build"
+    assert not needs_build(), "libksvd.so is older than its sources"
+    lib = _lib.load_library()
+    assert lib.ksvd_version() == 1
+
+
+def test_exports_every_declared_symbol():
+    lib = _lib.load_library()
+    syms = declared_symbols()
+    assert len(syms) >= 25
+    for s in syms:
+        assert hasattr(lib, s), s
+    # and the ctypes table binds exactly the header's surface
+    assert sorted(_lib.SIGNATURES) == syms
+
+
+def test_sm100a_code_in_library():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", str(LIB)], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout, out.stdout[:500]
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 13, 50, 120])
+def test_native_eig_matches_reference_kat(golden, n):
+    d, e = golden[f"eig/{n}/d"], golden[f"eig/{n}/e"]
+    theta, G = symtridiag_eig(SymTridiag(d, e))
+    tref, Gref = golden[f"eig/{n}/theta"], golden[f"eig/{n}/G"]
+    scale = max(np.max(np.abs(tref)), 1.0)
+    assert np.max(np.abs(theta - tref)) <= 1e-12 * scale
+    assert np.min(col_cos(G, Gref)) >= 1 - 1e-10
+    assert np.max(np.abs(G.T @ G - np.eye(n))) < 1e-12
+
+
+def test_native_eig_no_vectors_and_errors():
+    theta, G = symtridiag_eig(SymTridiag(np.array([1.0, 2.0]), np.array([0.5])), vectors=False)
+    assert G is None and theta.shape == (2,)
+    from paper_2104_10785_b200 import ConfigError
+
+    with pytest.raises(ConfigError):
+        symtridiag_eig(SymTridiag(np.zeros(0), np.zeros(0)))
+
+
+def test_no_cpu_fallback_without_gpu():
+    """On a host without a GPU every compute entry point fails loudly."""
+    import ctypes as C
+
+    lib = _lib.load_library()
+    n = C.c_int(0)
+    rc = lib.ksvd_device_count(C.byref(n))
+    if rc == 0 and n.value > 0:
+        pytest.skip("a GPU is visible")
+    from paper_2104_10785_b200 import fsvd
+
+    _lib.set_context(None)
+    with pytest.raises(RuntimeError):
+        fsvd(np.eye(4), k=2, r=1)

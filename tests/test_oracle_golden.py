@@ -1,0 +1,135 @@
+"""Pin the CPU oracle (oracle/krylov_oracle.py) against the reference.
+
+The golden vectors were produced by the reference package itself
+(tests/golden/make_golden.py); the known-answer cases restate the
+reference's own unit tests (test_bidiag.py, test_fsvd.py, test_rank.py).
+CPU only.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import krylov_oracle as O
+from tests.conftest import golden_cases
+from tests.golden.recipes import build_input, digest
+from tests.parity import (COS_TOL_F64, SIG_RTOL_F64, assert_scalars_close, col_cos,
+                          ortho_dev, recurrence_dev, sig_relerr)
+
+
+def test_start_vector_stream_bitwise(golden):
+    for key, q_ref in golden.items():
+        if not key.startswith("start/"):
+            continue
+        _, seed, m, mean, std = key.split("/")
+        g = O.gk_oracle(np.eye(int(m)), 1, seed=int(seed), start_mean=float(mean),
+                        start_std=float(std)) if int(m) <= 8 else None
+        q = float(mean) + float(std) * O.philox_stream(int(seed), O.GK_START).standard_normal(int(m))
+        q /= np.linalg.norm(q)
+        assert np.array_equal(q, q_ref)
+        if g is not None:
+            assert np.array_equal(g.Q[:, 0], q_ref)
+
+
+def test_inputs_reproduce(golden):
+    for parts in golden_cases(golden, "bidiag") + golden_cases(golden, "fsvd") + \
+            golden_cases(golden, "rank"):
+        A = build_input(parts[1])
+        assert digest(A) == parts[-1], parts
+
+
+def test_bidiag_cases(golden):
+    for parts in golden_cases(golden, "bidiag"):
+        key, recipe, k, seed, reorth = parts[0], parts[1], int(parts[2]), int(parts[3]), int(parts[4])
+        A = build_input(recipe)
+        g = O.gk_oracle(A, k, seed=seed, reorth_passes=reorth)
+        info = golden[key + "/info"]
+        assert [g.k_prime, int(g.terminated_early), int(g.degenerate), g.Q.shape[1],
+                g.P.shape[1]] == list(info), (recipe, info)
+        assert_scalars_close(g.alphas, g.betas, golden[key + "/alphas"], golden[key + "/betas"],
+                             what=recipe)
+        if key + "/Q" in golden and g.k_prime:
+            assert np.min(col_cos(g.Q, golden[key + "/Q"])) >= 1 - COS_TOL_F64
+            assert np.min(col_cos(g.P, golden[key + "/P"])) >= 1 - COS_TOL_F64
+        if g.k_prime:
+            tol = 1e-8 if reorth == 1 else 1e-10
+            assert ortho_dev(g.Q) < tol and ortho_dev(g.P) < 1e-10
+            assert recurrence_dev(A, g.alphas, g.betas, g.Q, g.P) < 1e-10
+
+
+def test_fsvd_cases(golden):
+    for parts in golden_cases(golden, "fsvd"):
+        key, recipe = parts[0], parts[1]
+        k, r, seed, eps, ortho = int(parts[2]), int(parts[3]), int(parts[4]), float(parts[5]), \
+            bool(int(parts[6]))
+        A = build_input(recipe)
+        res = O.fsvd_oracle(A, k, r, eps=eps, seed=seed, orthonormalize_u=ortho)
+        info = golden[key + "/info"]
+        assert [int(res.truncated), res.n_dropped, res.gk.k_prime, res.sigma.shape[0]] == \
+            list(info), (recipe, info)
+        assert sig_relerr(res.sigma, golden[key + "/sigma"]) <= SIG_RTOL_F64
+        nk = golden[key + "/U"].shape[1]
+        if nk:
+            assert np.min(col_cos(res.U[:, :nk], golden[key + "/U"])) >= 1 - COS_TOL_F64
+            assert np.min(col_cos(res.V[:, :nk], golden[key + "/V"])) >= 1 - COS_TOL_F64
+            # same sign convention -> same vectors, not just same lines
+            assert np.allclose(res.V[:, :nk], golden[key + "/V"], atol=1e-7)
+
+
+def test_rank_cases(golden):
+    for parts in golden_cases(golden, "rank"):
+        key, recipe, eps, mode, seed = parts[0], parts[1], float(parts[2]), parts[3], int(parts[4])
+        A = build_input(recipe)
+        rep = O.rank_oracle(A, eps=eps, mode=mode, seed=seed)
+        rank_ref, kp_ref = golden[key + "/info"]
+        assert rep.rank == rank_ref, recipe
+        assert rep.k_prime == kp_ref, recipe
+        ev = golden[key + "/eigenvalues"]
+        if ev.size:
+            assert np.max(np.abs(rep.eigenvalues - ev)) <= 1e-10 * ev[0]
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 13, 50, 120])
+def test_eig_kat(golden, n):
+    d, e = golden[f"eig/{n}/d"], golden[f"eig/{n}/e"]
+    theta, G = O.ql_eig(d, e)
+    tref, Gref = golden[f"eig/{n}/theta"], golden[f"eig/{n}/G"]
+    scale = max(np.max(np.abs(tref)), 1.0)
+    assert np.max(np.abs(theta - tref)) <= 1e-12 * scale
+    assert np.min(col_cos(G, Gref)) >= 1 - 1e-10
+
+
+# ---- the reference's hand-computable known answers ----
+def test_gram_hand_case():
+    d, off = O.gram_of([2.0, 3.0], [5.0, 4.0, 1.0])  # test_fsvd.py:26-31
+    assert np.array_equal(d, [20.0, 10.0]) and np.array_equal(off, [12.0])
+
+
+def test_eig_closed_forms():
+    theta, G = O.ql_eig(np.array([2.0, 1.0]), np.array([1.0]))  # test_fsvd.py:62-68
+    assert np.allclose(theta, [(3 + math.sqrt(5)) / 2, (3 - math.sqrt(5)) / 2], atol=1e-15)
+    theta, _ = O.ql_eig(np.zeros(2), np.ones(1))
+    assert np.allclose(theta, [1.0, -1.0], atol=1e-15)
+
+
+def test_identity_and_zero():
+    g = O.gk_oracle(np.eye(5), 5, seed=7)  # test_bidiag.py:41-54
+    assert g.k_prime == 1 and g.terminated_early and abs(g.alphas[0] - 1) < 1e-12
+    g = O.gk_oracle(np.zeros((6, 4)), 4, seed=3)  # test_bidiag.py:30-39
+    assert g.degenerate and g.Q.shape == (6, 1) and g.P.shape == (4, 0)
+
+
+def test_threshold_count():
+    theta = np.array([1.0, 1e-8, 1e-24])  # test_rank.py:13-18
+    assert O.threshold_count(theta, 1e-8, "absolute") == (1, 1e-8)
+    assert O.threshold_count(np.array([4.0, 1e-6]), 1e-2, "relative") == (1, 1e-4 * 4.0)
+    assert O.threshold_count(np.zeros(0), 1e-8, "relative") == (0, 0.0)
+
+
+def test_readme_known_answer():
+    # reference README:58-61 -- 1000x1000 rank 100 at seed 0 -> rank 100, k' 102
+    from paper_2104_10785_b200.synth import low_rank_synth
+
+    rep = O.rank_oracle(low_rank_synth(1000, 1000, 100, seed=0), seed=0)
+    assert (rep.rank, rep.k_prime) == (100, 102)
