@@ -60,6 +60,36 @@ def recurrence_dev(A, alphas, betas, Q, P):
     return dev / max(np.linalg.norm(A), 1e-300)
 
 
+def gram_eigs(alphas, betas):
+    """Ritz values theta of B^T B (dense eigvalsh; test-side helper)."""
+    k = len(alphas)
+    if k == 0:
+        return np.zeros(0)
+    B = bidiagonal(alphas, betas)
+    return np.sort(np.linalg.eigvalsh(B.T @ B))[::-1]
+
+
+def assert_gk_match(a, b, kp, ra, rb, rkp, head=8, kp_slack=2, what=""):
+    """Parity of two GK runs on the same input with different summation
+    orders.  The per-step scalars are forward-unstable once the Krylov space
+    nears the numerical rank (the recurrence amplifies rounding; measured
+    here and in SURVEY.md 8(c) probe 5), so the contract is: k' within a
+    small window, the leading `head` alphas/betas to 1e-10, and the Ritz
+    values of B^T B -- the quantities fsvd/estimate_rank consume -- to
+    1e-10 of theta_1."""
+    assert abs(kp - rkp) <= kp_slack, (what, kp, rkp)
+    h = min(head, len(a), len(ra))
+    if h:
+        scale = np.max(np.abs(ra))
+        assert np.max(np.abs(a[:h] - ra[:h])) <= SIG_RTOL_F64 * scale, (what, "alphas")
+        bscale = np.max(np.abs(rb))
+        assert np.max(np.abs(b[:h + 1] - rb[:h + 1])) <= SIG_RTOL_F64 * bscale, (what, "betas")
+    th, rth = gram_eigs(a, b), gram_eigs(ra, rb)
+    nt = min(len(th), len(rth))
+    if nt:
+        assert np.max(np.abs(th[:nt] - rth[:nt])) <= SIG_RTOL_F64 * rth[0], (what, "theta")
+
+
 def assert_scalars_close(ours_a, ours_b, ref_a, ref_b, rtol=SIG_RTOL_F64, what=""):
     assert len(ours_a) == len(ref_a), (what, len(ours_a), len(ref_a))
     assert len(ours_b) == len(ref_b), (what, len(ours_b), len(ref_b))
