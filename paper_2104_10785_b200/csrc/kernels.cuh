@@ -10,6 +10,7 @@
 // breakdown / non-finite value has been recorded, so the host can enqueue
 // several steps ahead without synchronising (bidiag.py:151-178 loop).
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -37,6 +38,17 @@ struct DevState {
                   // halts at the same step and issues the same collectives
 };
 
+// Progress word in mapped (zero-copy) host memory, written by the norm tests
+// of the GK loop: prog = 2*step + side (side 0: beta test, 1: alpha test);
+// a breakdown also records status and halt_step.  The host paces its
+// run-ahead on it instead of per-step device->host copies.
+struct HostProg {
+  int prog;
+  int halt_step;
+  int status;
+  int pad;
+};
+
 __device__ __forceinline__ bool halted(const DevState* st) {
   return *reinterpret_cast<const volatile int*>(&st->status) != ST_RUNNING;
 }
@@ -45,6 +57,39 @@ __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// Sum 8 per-lane values across the warp at once ("transpose" butterfly:
+// 9 shuffles instead of 8 x 5).  On return lane l holds the total of value
+// index ((l>>4)&1)*4 + ((l>>3)&1)*2 + ((l>>2)&1); lanes with (l & 3) == 0
+// own distinct indices.  The combination order is fixed (deterministic).
+__device__ __forceinline__ double warp_sum8(double (&v)[8]) {
+  const int lane = threadIdx.x & 31;
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double send = b4 ? v[k] : v[k + 4];
+    const double keep = b4 ? v[k + 4] : v[k];
+    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double send = b3 ? v[k] : v[k + 2];
+    const double keep = b3 ? v[k + 2] : v[k];
+    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  {
+    const double send = b2 ? v[0] : v[1];
+    const double keep = b2 ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  double t = v[0];
+  t += __shfl_xor_sync(0xffffffffu, t, 2);
+  t += __shfl_xor_sync(0xffffffffu, t, 1);
+  return t;
+}
+__device__ __forceinline__ int warp_sum8_index(int lane) {
+  return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -80,103 +125,76 @@ __device__ __forceinline__ void flag_nonfinite(DevState* st, double v, int step)
 }
 
 // ---------------------------------------------------------------------------
-// gemv_n:  w = A p - alpha q_prev          (bidiag.py:152, linops.py:161)
+// gemv_n, column-chunked (k_gemv_n2): w = A p   (bidiag.py:152)
 //
-// Grid (blocks_per_chunk, nchunks).  Chunk y owns columns
-// [y*chunk_vecs*V, ...); its slice of p (optionally p = p_src / *p_scale,
-// the deferred normalisation P[:, i-1] = z / alpha, bidiag.py:177) is staged
-// in shared memory once per CTA and reused for every row the CTA streams.
-// Each warp owns R consecutive rows at a time; lanes stride the row with
-// 16-byte loads, U loads in flight per row.  nchunks == 1 writes w with the
-// fused -alpha*q epilogue; otherwise per-chunk partial row sums go to
-// `out` (chunk-major) and k_gemv_n_finalize adds them in chunk order.
-template <typename TA, int R, int U>
+// Each warp owns one column chunk of 32*U 16-byte vectors and a range of
+// rows.  Its slice of p (p = p_src / *p_scale, the deferred normalisation
+// of P[:, i-1]) is loaded once into registers; the warp then streams 8 rows
+// per iteration (8*U independent 16-byte loads per lane in flight), forms
+// the 8 row partials, and reduces them across the warp with one 9-shuffle
+// transpose butterfly (warp_sum8).  Warps of a CTA take consecutive chunks
+// of the same rows, so a CTA reads long contiguous row segments.  Partials
+// per (chunk, row) go to part[chunk*m + row]; k_gemv_n_finalize adds them
+// in chunk order and applies - alpha q.
+template <typename TA, int U>
 __global__ void __launch_bounds__(kThreads)
-k_gemv_n(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
-         int chunk_vecs, const double* __restrict__ p_src,
-         const double* __restrict__ p_scale, double* __restrict__ p_dst,
-         int64_t n_true, double* __restrict__ out, int64_t out_ld,
-         const double* __restrict__ qprev, const double* __restrict__ alpha,
-         DevState* st, int step, int64_t groups_per_warp) {
+k_gemv_n2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nchunks,
+          int64_t rows_per_warp, const double* __restrict__ p_src,
+          const double* __restrict__ p_scale, double* __restrict__ p_dst, int64_t n_true,
+          double* __restrict__ part, const DevState* st) {
   if (halted(st)) return;
   constexpr int V = AVec<TA>::V;
-  extern __shared__ double p_s[];
-  const int chunk = blockIdx.y;
-  const int64_t v0 = (int64_t)chunk * chunk_vecs;
-  const int nv = (int)min((int64_t)chunk_vecs, nvec - v0);
-  const int64_t c0 = v0 * V;
-  const double scale = p_scale ? *p_scale : 1.0;
-  for (int e = threadIdx.x; e < nv * V; e += kThreads) {
-    const int64_t col = c0 + e;
-    double pv = col < n_true ? p_src[col] : 0.0;
-    if (p_scale) {
-      pv = pv / scale;
-      if (blockIdx.x == 0 && p_dst && col < n_true) p_dst[col] = pv;
-    }
-    p_s[e] = pv;
-  }
-  __syncthreads();
-
+  constexpr int CW = 32 * U;
   const int lane = threadIdx.x & 31;
-  const int64_t gwarp = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const int64_t ngroups = (m + R - 1) / R;
-  const double a_ = alpha ? *alpha : 0.0;
-  const int64_t g_begin = gwarp * groups_per_warp;
-  const int64_t g_end = min(ngroups, g_begin + groups_per_warp);
-  for (int64_t g = g_begin; g < g_end; ++g) {
-    const int64_t r0 = g * R;
-    const TA* rowp[R];
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int chunk = (int)(gw % nchunks);
+  const int64_t rseg = gw / nchunks;
+  const int64_t r_begin = rseg * rows_per_warp;
+  if (r_begin >= m) return;
+  const int64_t r_end = min(m, r_begin + rows_per_warp);
+  const double scale = p_scale ? *p_scale : 1.0;
+  double pv[U][V];
+  bool live[U];
 #pragma unroll
-    for (int r = 0; r < R; ++r) rowp[r] = A + min(r0 + r, m - 1) * lda + c0;
-    double acc[R][V];
+  for (int u = 0; u < U; ++u) {
+    const int64_t vi = (int64_t)chunk * CW + u * 32 + lane;
+    live[u] = vi < nvec;
 #pragma unroll
-    for (int r = 0; r < R; ++r)
+    for (int k = 0; k < V; ++k) {
+      const int64_t col = vi * V + k;
+      double x = (live[u] && col < n_true) ? p_src[col] : 0.0;
+      if (p_scale) {
+        x = x / scale;
+        if (rseg == 0 && p_dst && live[u] && col < n_true) p_dst[col] = x;
+      }
+      pv[u][k] = x;
+    }
+  }
+  const TA* base = A + ((int64_t)chunk * CW + lane) * V;
+  for (int64_t r = r_begin; r < r_end; r += 8) {
+    double v[8];
+    AVec<TA> a[8][U];
 #pragma unroll
-      for (int k = 0; k < V; ++k) acc[r][k] = 0.0;
-    int v = lane;
-    for (; v + (U - 1) * 32 < nv; v += U * 32) {
-      AVec<TA> a[U][R];
+    for (int rr = 0; rr < 8; ++rr) {
+      const int64_t row = min(r + rr, r_end - 1);  // clamp: duplicate rows are discarded
 #pragma unroll
       for (int u = 0; u < U; ++u)
+        if (live[u]) a[rr][u].load(base + row * lda + u * 32 * V);
+    }
 #pragma unroll
-        for (int r = 0; r < R; ++r) a[u][r].load(rowp[r] + (int64_t)(v + u * 32) * V);
+    for (int rr = 0; rr < 8; ++rr) {
+      double s = 0.0;
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const double* pp = p_s + (v + u * 32) * V;
+      for (int u = 0; u < U; ++u)
+        if (live[u]) {
 #pragma unroll
-        for (int k = 0; k < V; ++k) {
-          const double pk = pp[k];
-#pragma unroll
-          for (int r = 0; r < R; ++r) acc[r][k] = fma(a[u][r].get(k), pk, acc[r][k]);
+          for (int k = 0; k < V; ++k) s = fma(a[rr][u].get(k), pv[u][k], s);
         }
-      }
+      v[rr] = s;
     }
-    for (; v < nv; v += 32) {
-      AVec<TA> a[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) a[r].load(rowp[r] + (int64_t)v * V);
-      const double* pp = p_s + v * V;
-#pragma unroll
-      for (int k = 0; k < V; ++k)
-#pragma unroll
-        for (int r = 0; r < R; ++r) acc[r][k] = fma(a[r].get(k), pp[k], acc[r][k]);
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      double s = acc[r][0];
-#pragma unroll
-      for (int k = 1; k < V; ++k) s += acc[r][k];
-      s = warp_sum(s);
-      if (lane == r && r0 + r < m) {
-        if (out_ld == 0) {  // direct epilogue
-          const double w = qprev ? s - a_ * qprev[r0 + r] : s;
-          out[r0 + r] = w;
-          flag_nonfinite(st, w, step);
-        } else {
-          out[(int64_t)chunk * out_ld + r0 + r] = s;
-        }
-      }
-    }
+    const double t = warp_sum8(v);
+    const int64_t row = r + warp_sum8_index(lane);
+    if ((lane & 3) == 0 && row < r_end) part[(int64_t)chunk * m + row] = t;
   }
 }
 
@@ -200,15 +218,17 @@ k_gemv_n_finalize(const double* __restrict__ part, int64_t part_ld, int nchunks,
 // gemv_t:  partial z = A^T q over a row split  (bidiag.py:169, linops.py:164)
 //
 // Column reduction of row-major A without a transposed copy.  Grid
-// (ncoltiles, nsplit).  Each thread owns one 16-byte column vector
-// (V columns) of a 256-vector tile and accumulates V f64 sums down the
-// rows of its split, U rows in flight.  q for the split is staged through
-// shared memory in blocks of kQB rows (optionally q = q_src / *q_scale: the
-// deferred normalisation q_{i+1} = w / beta, bidiag.py:165, written to
-// q_dst by tile-0 CTAs).  Partials of split s go to part[s*ldz + col];
-// k_gemv_t_finalize adds the splits in order.
+// (ncoltiles, nsplit).  The CTA's 256 threads form RG row groups of
+// TPG = 256/RG threads; each thread owns one 16-byte column vector (V
+// columns) of the CTA's TPG-vector tile and accumulates V f64 sums over the
+// rows of its group (rows g, g+RG, ... of the split, U rows in flight).  q
+// for the split is staged through shared memory in blocks of kQB rows
+// (optionally q = q_src / *q_scale: the deferred normalisation
+// q_{i+1} = w / beta, bidiag.py:165, written to q_dst by tile-0 CTAs).  The
+// RG group sums are combined in fixed order in shared memory and the split
+// partial goes to part[s*ldz + col]; k_gemv_t_finalize adds the splits.
 constexpr int kQB = 1024;
-template <typename TA, int U>
+template <typename TA, int U, int RG>
 __global__ void __launch_bounds__(kThreads)
 k_gemv_t(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
          int64_t rows_per_split, const double* __restrict__ q_src,
@@ -216,8 +236,11 @@ k_gemv_t(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
          double* __restrict__ part, int64_t ldz, const DevState* st) {
   if (halted(st)) return;
   constexpr int V = AVec<TA>::V;
+  constexpr int TPG = kThreads / RG;
   __shared__ double q_s[kQB];
-  const int64_t vcol = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  __shared__ double red[RG > 1 ? RG : 1][RG > 1 ? TPG * V : 1];
+  const int g = threadIdx.x / TPG, t = threadIdx.x % TPG;
+  const int64_t vcol = (int64_t)blockIdx.x * TPG + t;
   const bool active = vcol < nvec;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_split;
   const int64_t r1 = min(m, r0 + rows_per_split);
@@ -240,19 +263,19 @@ k_gemv_t(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
     __syncthreads();
     if (!active) continue;
     const TA* p = base + rb * lda;
-    int r = 0;
-    for (; r + U <= nr; r += U) {
+    int r = g;
+    for (; r + (U - 1) * RG < nr; r += U * RG) {
       AVec<TA> a[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) a[u].load(p + (int64_t)(r + u) * lda);
+      for (int u = 0; u < U; ++u) a[u].load(p + (int64_t)(r + u * RG) * lda);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const double qv = q_s[r + u];
+        const double qv = q_s[r + u * RG];
 #pragma unroll
         for (int k = 0; k < V; ++k) acc[k] = fma(a[u].get(k), qv, acc[k]);
       }
     }
-    for (; r < nr; ++r) {
+    for (; r < nr; r += RG) {
       AVec<TA> a;
       a.load(p + (int64_t)r * lda);
       const double qv = q_s[r];
@@ -260,28 +283,53 @@ k_gemv_t(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
       for (int k = 0; k < V; ++k) acc[k] = fma(a.get(k), qv, acc[k]);
     }
   }
-  if (active) {
+  if constexpr (RG > 1) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) red[g][t * V + k] = acc[k];
+    __syncthreads();
+    if (g == 0 && active) {
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        double s = red[0][t * V + k];
+#pragma unroll
+        for (int gg = 1; gg < RG; ++gg) s += red[gg][t * V + k];
+        acc[k] = s;
+      }
+    }
+  }
+  if (g == 0 && active) {
     double* dst = part + (int64_t)blockIdx.y * ldz + vcol * V;
 #pragma unroll
     for (int k = 0; k < V; ++k) dst[k] = acc[k];
   }
 }
 
-// z[j] = sum_s part[s][j] (- beta p[j]);  zero in the padding [n, n_pad)
+// z[j] = sum_s part[s][j] (- beta p[j]); zero in the padding [n, n_pad).
+// CTA = 32 columns x 8 split groups: group g adds splits g, g+8, ...
+// (coalesced 256-byte rows of partials), then the groups are combined in
+// fixed order.
 __global__ void __launch_bounds__(kThreads)
 k_gemv_t_finalize(const double* __restrict__ part, int64_t ldz, int nsplit,
                   int64_t n, int64_t n_pad, const double* __restrict__ beta,
                   const double* __restrict__ pprev, double* __restrict__ z,
                   DevState* st, int step, int check) {
   if (halted(st)) return;
-  const int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  if (j >= n_pad) return;
+  __shared__ double red[kWarps][32];
+  const int c = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t j = (int64_t)blockIdx.x * 32 + c;
+  double s = 0.0;
+  if (j < n)
+    for (int k = g; k < nsplit; k += kWarps) s += part[(int64_t)k * ldz + j];
+  red[g][c] = s;
+  __syncthreads();
+  if (g != 0 || j >= n_pad) return;
   if (j >= n) {
     z[j] = 0.0;
     return;
   }
-  double s = part[j];
-  for (int k = 1; k < nsplit; ++k) s += part[(int64_t)k * ldz + j];
+  s = red[0][c];
+#pragma unroll
+  for (int w = 1; w < kWarps; ++w) s += red[w][c];
   if (pprev) s = s - (*beta) * pprev[j];
   z[j] = s;
   if (check) flag_nonfinite(st, s, step);
@@ -302,230 +350,589 @@ k_axpy_check(double* __restrict__ z, const double* __restrict__ beta,
 
 // ---------------------------------------------------------------------------
 // CGS2 (bidiag.py:154-155, 171-172):  c = B^T x ; x -= B c ; (twice)
-// B is a basis of `ncols` columns, each contiguous (ldb doubles apart).
-// A CTA owns 256*E consecutive rows; the partial dot of column j over row
-// block b lands in part[j*nrb + b] and k_reduce_cols adds the blocks.
-constexpr int kJ = 8;  // basis columns per CTA in the dot kernel
+//
+// B is a basis of `ncols` columns, each contiguous (ldb doubles apart), held
+// in HBM/L2.  One kernel serves every pass: a CTA owns 32*RPL consecutive
+// rows (lane = row, RPL rows per lane), its 8 warps split the columns
+// (warp w takes j = w, w+8, ...), so every column read is a coalesced
+// 256*RPL-byte segment and all loads of a warp are independent.
+//   mode & kUpdate : x -= B c   (per-warp partial sums combined across the
+//                    8 warps in fixed order through shared memory)
+//   mode & kDot    : part[j*nrb + b] = sum_{rows of b} B[j][r] x[r] -- the
+//                    coefficients of the NEXT pass; the CTA's B tile was
+//                    just read by the update, so this re-read hits L1
+//   mode & kNorm   : part[b] = sum_{rows of b} x[r]^2
+// k_reduce_part adds the row blocks (fixed order) into c / the norm.
+constexpr int kUpdate = 1, kDot = 2, kNorm = 4;
 
-template <int E>
+template <int RPL>
 __global__ void __launch_bounds__(kThreads)
-k_cgs_dot(const double* __restrict__ B, int64_t ldb, int ncols,
-          const double* __restrict__ x, int64_t L, double* __restrict__ part,
-          int nrb, const DevState* st) {
+k_cgs_rows(const double* __restrict__ B, int64_t ldb, int ncols,
+           const double* __restrict__ c, double* __restrict__ x, int64_t L,
+           int mode, double* __restrict__ part, int nrb, const DevState* st) {
   if (halted(st)) return;
-  __shared__ double red[kWarps][kJ];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t rbase = (int64_t)blockIdx.x * (kThreads * E) + tid;
-  double xr[E];
+  constexpr int ROWS = 32 * RPL;
+  __shared__ double tred[kWarps][ROWS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * ROWS + lane;
+  double xv[RPL];
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int64_t r = rbase + e * kThreads;
-    xr[e] = r < L ? x[r] : 0.0;
+  for (int e = 0; e < RPL; ++e) {
+    const int64_t r = r0 + 32 * e;
+    xv[e] = r < L ? x[r] : 0.0;
   }
-  const int j0 = blockIdx.y * kJ;
-  double s[kJ];
+  if (mode & kUpdate) {
+    double t[RPL];
 #pragma unroll
-  for (int jj = 0; jj < kJ; ++jj) {
-    s[jj] = 0.0;
-    if (j0 + jj < ncols) {
-      const double* col = B + (int64_t)(j0 + jj) * ldb;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int64_t r = rbase + e * kThreads;
-        if (r < L) s[jj] = fma(col[r], xr[e], s[jj]);
-      }
-    }
-  }
-#pragma unroll
-  for (int jj = 0; jj < kJ; ++jj) s[jj] = warp_sum(s[jj]);
-  if (lane == 0) {
-#pragma unroll
-    for (int jj = 0; jj < kJ; ++jj) red[warp][jj] = s[jj];
-  }
-  __syncthreads();
-  if (tid < kJ && j0 + tid < ncols) {
-    double t = red[0][tid];
-#pragma unroll
-    for (int w = 1; w < kWarps; ++w) t += red[w][tid];
-    part[(int64_t)(j0 + tid) * nrb + blockIdx.x] = t;
-  }
-}
-
-// x -= B c, then (mode 1) partial dots of the updated x against B for the
-// next CGS pass, or (mode 2) the partial ||x||^2, or (mode 0) nothing.
-constexpr int kCChunk = 1024;
-template <int E>
-__global__ void __launch_bounds__(kThreads)
-k_cgs_update(const double* __restrict__ B, int64_t ldb, int ncols,
-             const double* __restrict__ c, double* __restrict__ x, int64_t L,
-             int mode, double* __restrict__ part, int nrb, const DevState* st) {
-  if (halted(st)) return;
-  __shared__ double cs[kCChunk];
-  __shared__ double red[kWarps][kJ];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t rbase = (int64_t)blockIdx.x * (kThreads * E) + tid;
-  double xr[E], t[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int64_t r = rbase + e * kThreads;
-    xr[e] = r < L ? x[r] : 0.0;
-    t[e] = 0.0;
-  }
-  for (int j0 = 0; j0 < ncols; j0 += kCChunk) {
-    const int nc = min(kCChunk, ncols - j0);
-    __syncthreads();
-    for (int e = tid; e < nc; e += kThreads) cs[e] = c[j0 + e];
-    __syncthreads();
+    for (int e = 0; e < RPL; ++e) t[e] = 0.0;
 #pragma unroll 4
-    for (int jj = 0; jj < nc; ++jj) {
-      const double cj = cs[jj];
-      const double* col = B + (int64_t)(j0 + jj) * ldb;
+    for (int j = warp; j < ncols; j += kWarps) {
+      const double cj = c[j];
+      const double* col = B + (int64_t)j * ldb;
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int64_t r = rbase + e * kThreads;
+      for (int e = 0; e < RPL; ++e) {
+        const int64_t r = r0 + 32 * e;
         if (r < L) t[e] = fma(col[r], cj, t[e]);
       }
     }
-  }
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int64_t r = rbase + e * kThreads;
-    xr[e] = xr[e] - t[e];
-    if (r < L) x[r] = xr[e];
+    for (int e = 0; e < RPL; ++e) tred[warp][lane + 32 * e] = t[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < RPL; ++e) {
+      double s = tred[0][lane + 32 * e];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) s += tred[w][lane + 32 * e];
+      xv[e] = xv[e] - s;
+      const int64_t r = r0 + 32 * e;
+      if (warp == 0 && r < L) x[r] = xv[e];
+    }
   }
-  if (mode == 2) {
+  if (mode & kDot) {
+#pragma unroll 2
+    for (int j = warp; j < ncols; j += kWarps) {
+      const double* col = B + (int64_t)j * ldb;
+      double s = 0.0;
+#pragma unroll
+      for (int e = 0; e < RPL; ++e) {
+        const int64_t r = r0 + 32 * e;
+        if (r < L) s = fma(col[r], xv[e], s);
+      }
+      s = warp_sum(s);
+      if (lane == 0) part[(int64_t)j * nrb + blockIdx.x] = s;
+    }
+  }
+  if ((mode & kNorm) && warp == 0) {
     double s = 0.0;
 #pragma unroll
-    for (int e = 0; e < E; ++e) s = fma(xr[e], xr[e], s);
+    for (int e = 0; e < RPL; ++e) s = fma(xv[e], xv[e], s);
     s = warp_sum(s);
-    if (lane == 0) red[warp][0] = s;
-    __syncthreads();
-    if (tid == 0) {
-      double tt = red[0][0];
-#pragma unroll
-      for (int w = 1; w < kWarps; ++w) tt += red[w][0];
-      part[blockIdx.x] = tt;
-    }
-  } else if (mode == 1) {
-    for (int j0 = 0; j0 < ncols; j0 += kJ) {
-      double s[kJ];
-#pragma unroll
-      for (int jj = 0; jj < kJ; ++jj) {
-        s[jj] = 0.0;
-        if (j0 + jj < ncols) {
-          const double* col = B + (int64_t)(j0 + jj) * ldb;
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const int64_t r = rbase + e * kThreads;
-            if (r < L) s[jj] = fma(col[r], xr[e], s[jj]);
-          }
-        }
-      }
-#pragma unroll
-      for (int jj = 0; jj < kJ; ++jj) s[jj] = warp_sum(s[jj]);
-      __syncthreads();
-      if (lane == 0) {
-#pragma unroll
-        for (int jj = 0; jj < kJ; ++jj) red[warp][jj] = s[jj];
-      }
-      __syncthreads();
-      if (tid < kJ && j0 + tid < ncols) {
-        double tt = red[0][tid];
-#pragma unroll
-        for (int w = 1; w < kWarps; ++w) tt += red[w][tid];
-        part[(int64_t)(j0 + tid) * nrb + blockIdx.x] = tt;
-      }
-    }
+    if (lane == 0) part[blockIdx.x] = s;
   }
 }
 
-// ||x||^2 partials (pass-less norm, used when the basis is empty)
-template <int E>
-__global__ void __launch_bounds__(kThreads)
-k_sumsq(const double* __restrict__ x, int64_t L, double* __restrict__ part,
-        const DevState* st) {
-  if (halted(st)) return;
-  __shared__ double red[kWarps];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t rbase = (int64_t)blockIdx.x * (kThreads * E) + tid;
-  double s = 0.0;
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int64_t r = rbase + e * kThreads;
-    const double v = r < L ? x[r] : 0.0;
-    s = fma(v, v, s);
-  }
-  s = warp_sum(s);
-  if (lane == 0) red[warp] = s;
+// fixed-order block sum of v over the 256 threads (result valid in thread 0)
+__device__ __forceinline__ double block_sum(double v, double* red8) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __syncthreads();
-  if (tid == 0) {
-    double t = red[0];
+  if (lane == 0) red8[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0) {
+    t = red8[0];
 #pragma unroll
-    for (int w = 1; w < kWarps; ++w) t += red[w];
-    part[blockIdx.x] = t;
+    for (int w = 1; w < kWarps; ++w) t += red8[w];
   }
+  return t;
 }
 
-// out[j] = sum_b part[j*nrb + b], one warp per column, fixed order
+// out[j] = sum_b part[j*nrb + b]; one CTA per column, fixed order
 __global__ void __launch_bounds__(kThreads)
-k_reduce_cols(const double* __restrict__ part, int nrb, int ncols,
-              double* __restrict__ out, const DevState* st) {
+k_reduce_part(const double* __restrict__ part, int nrb, double* __restrict__ out,
+              const DevState* st) {
   if (halted(st)) return;
-  const int j = blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (j >= ncols) return;
-  const double* p = part + (int64_t)j * nrb;
+  __shared__ double red8[kWarps];
+  const double* p = part + (int64_t)blockIdx.x * nrb;
   double s = 0.0;
-  for (int b = lane; b < nrb; b += 32) s += p[b];
-  s = warp_sum(s);
-  if (lane == 0) out[j] = s;
+  for (int b = threadIdx.x; b < nrb; b += kThreads) s += p[b];
+  s = block_sum(s, red8);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
 }
 
 // Norm test (bidiag.py:156-158, 173-174; fsvd.py:151-152).
 // nrb > 0: s = sum part[0..nrb) and the local non-finite flag (single rank).
 // nrb == 0: s = red[0], flag = red[1] (already all-reduced by the caller).
 // nrm = sqrt(s) -> *slot; non-finite -> ST_NONFINITE; nrm < eps -> `code`.
-__global__ void k_norm_test(const double* __restrict__ part, int nrb,
-                            const double* __restrict__ red, double eps,
-                            double* __restrict__ slot, DevState* st, int step,
-                            int code) {
+__global__ void __launch_bounds__(kThreads)
+k_norm_test(const double* __restrict__ part, int nrb, const double* __restrict__ red,
+            double eps, double* __restrict__ slot, DevState* st, int step, int code,
+            HostProg* hp, int side) {
   if (halted(st)) return;
-  const int lane = threadIdx.x;
+  __shared__ double red8[kWarps];
   double s = 0.0, flag = 0.0;
   if (nrb > 0) {
-    for (int b = lane; b < nrb; b += 32) s += part[b];
-    s = warp_sum(s);
+    for (int b = threadIdx.x; b < nrb; b += kThreads) s += part[b];
+    s = block_sum(s, red8);
     flag = st->nonfinite ? 1.0 : 0.0;
   } else {
     s = red[0];
     flag = red[1];
   }
-  if (lane == 0) {
+  if (threadIdx.x == 0) {
     const double nrm = sqrt(s);
     *slot = nrm;
-    if (flag != 0.0 || !isfinite(nrm)) {
-      st->status = ST_NONFINITE;
+    int stop = ST_RUNNING;
+    if (flag != 0.0 || !isfinite(nrm)) stop = ST_NONFINITE;
+    else if (nrm < eps) stop = code;
+    if (stop != ST_RUNNING) {
+      st->status = stop;
       st->kprime = step;
       st->where = step;
-    } else if (nrm < eps) {
-      st->status = code;
-      st->kprime = step;
-      st->where = step;
+    }
+    // publish to the host: breakdowns always, otherwise only the step's last
+    // test (side 1); a release store orders the status words before prog
+    if (hp && (stop != ST_RUNNING || side == 1)) {
+      volatile HostProg* h = hp;
+      if (stop != ST_RUNNING) {
+        h->status = stop;
+        h->halt_step = step;
+      }
+      asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(&hp->prog),
+                   "r"(2 * step + side)
+                   : "memory");
     }
   }
 }
 
 // red[0] = sum part[0..nrb), red[1] = local non-finite flag (pre all-reduce)
-__global__ void k_norm_prep(const double* __restrict__ part, int nrb,
-                            double* __restrict__ red, const DevState* st) {
+__global__ void __launch_bounds__(kThreads)
+k_norm_prep(const double* __restrict__ part, int nrb, double* __restrict__ red,
+            const DevState* st) {
   if (halted(st)) return;
-  const int lane = threadIdx.x;
+  __shared__ double red8[kWarps];
   double s = 0.0;
-  for (int b = lane; b < nrb; b += 32) s += part[b];
-  s = warp_sum(s);
-  if (lane == 0) {
+  for (int b = threadIdx.x; b < nrb; b += kThreads) s += part[b];
+  s = block_sum(s, red8);
+  if (threadIdx.x == 0) {
     red[0] = s;
     red[1] = st->nonfinite ? 1.0 : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused CGS2 for one rank (bidiag.py:154-156, 171-173): ONE cooperative
+// kernel per orthogonalisation instead of six launches.  Every CTA owns a
+// contiguous slab of rows; phases are separated by a grid barrier:
+//
+//   [0] optional gemv_t finalisation: x = sum_splits(part) - beta p
+//   [1] partial c = B^T x over the slab           -> part[j*G + b]
+//   [2] c[j] = sum_b part[j*G + b]  (columns spread over all warps)
+//   [3] x -= B c, fused with the next pass's partials (or ||x||^2)
+//   ... [2],[3] repeated per pass ...
+//   [4] CTA 0: beta / alpha = sqrt(sum_b part[b]); breakdown test
+//
+// All sums run in a fixed order, independent of scheduling.  The grid is
+// launched cooperatively (co-residency guaranteed by the driver) and the
+// barrier is a counter/generation pair in global memory.
+struct CgsCoopArgs {
+  const double* B;
+  int64_t ldb;
+  int ncols;
+  double* x;
+  int64_t L;
+  int rows_per_cta;
+  int passes;  // 0: norm only
+  double eps;
+  double* slot;
+  DevState* st;
+  int step, code;
+  HostProg* hp;
+  int side;
+  double* part;   // >= ncols * G
+  double* c;      // >= ncols
+  unsigned* bar;  // {count, generation}
+  // phase 0 (nullable fpart): x[r] = sum_s fpart[s*fld + r] - (*fbeta) fp[r]
+  const double* fpart;
+  int64_t fld;
+  int fnsplit;
+  const double* fbeta;
+  const double* fp;
+  unsigned long long* tdbg;  // nullable: phase timing of CTA 0
+};
+
+// Grid-wide barrier of the cooperative launch (cooperative_groups: ~1.2 us
+// on 148 SMs, measured by tools/barrier_bench.cu, vs ~2.3 us for a plain
+// counter/generation barrier).
+__device__ __forceinline__ void grid_barrier(unsigned* /*bar*/, unsigned /*nblocks*/) {
+  cooperative_groups::this_grid().sync();
+}
+
+// phase timestamps of CTA 0 (debug builds of the timing breakdown)
+__device__ __forceinline__ void phase_mark(unsigned long long* t, int k, unsigned long long& last) {
+  if (t && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (k > 0) atomicAdd(t + k, now - last);
+    last = now;
+  }
+}
+
+// columns of `part` (ncols x G, column-major in b) summed into c; warps of
+// the whole grid take columns round-robin
+__device__ __forceinline__ void coop_reduce_cols(const double* part, int ncols, int G,
+                                                 double* c) {
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int nw = gridDim.x * kWarps;
+  for (int j = gw; j < ncols; j += nw) {
+    const double* p = part + (int64_t)j * G;
+    double s = 0.0;
+    for (int b = lane; b < G; b += 32) s += __ldcg(p + b);
+    s = warp_sum(s);
+    if (lane == 0) c[j] = s;
+  }
+}
+
+template <int RPL>
+__global__ void __launch_bounds__(kThreads)
+k_cgs2_coop(CgsCoopArgs a) {
+  if (halted(a.st)) return;
+  constexpr int CH = 32 * RPL;  // rows per chunk
+  extern __shared__ double colacc[];  // ncols (dot accumulators)
+  __shared__ double tred[kWarps][CH];
+  __shared__ double nacc;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned G = gridDim.x;
+  const int64_t s0 = (int64_t)blockIdx.x * a.rows_per_cta;
+  const int64_t s1 = min(a.L, s0 + a.rows_per_cta);
+
+  // [0] finalisation of the split partial sums of A^T q
+  if (a.fpart) {
+    for (int64_t r = s0 + threadIdx.x; r < s1; r += kThreads) {
+      double v = 0.0;
+      for (int k = 0; k < a.fnsplit; ++k) v += a.fpart[(int64_t)k * a.fld + r];
+      if (a.fp) v = v - (*a.fbeta) * a.fp[r];
+      a.x[r] = v;
+      flag_nonfinite(a.st, v, a.step);
+    }
+    __syncthreads();
+  }
+
+  // one sweep over the slab: optional update with c, then dot or norm
+  auto sweep = [&](bool update, bool dot) {
+    if (dot)
+      for (int j = threadIdx.x; j < a.ncols; j += kThreads) colacc[j] = 0.0;
+    double nsum = 0.0;
+    __syncthreads();
+    for (int64_t r0 = s0; r0 < s1; r0 += CH) {
+      double xv[RPL];
+#pragma unroll
+      for (int e = 0; e < RPL; ++e) {
+        const int64_t r = r0 + lane + 32 * e;
+        xv[e] = r < s1 ? a.x[r] : 0.0;
+      }
+      if (update) {
+        double t[RPL];
+#pragma unroll
+        for (int e = 0; e < RPL; ++e) t[e] = 0.0;
+#pragma unroll 4
+        for (int j = warp; j < a.ncols; j += kWarps) {
+          const double cj = __ldcg(a.c + j);
+          const double* col = a.B + (int64_t)j * a.ldb;
+#pragma unroll
+          for (int e = 0; e < RPL; ++e) {
+            const int64_t r = r0 + lane + 32 * e;
+            if (r < s1) t[e] = fma(col[r], cj, t[e]);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < RPL; ++e) tred[warp][lane + 32 * e] = t[e];
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < RPL; ++e) {
+          double s = tred[0][lane + 32 * e];
+#pragma unroll
+          for (int w = 1; w < kWarps; ++w) s += tred[w][lane + 32 * e];
+          xv[e] = xv[e] - s;
+          const int64_t r = r0 + lane + 32 * e;
+          if (warp == 0 && r < s1) a.x[r] = xv[e];
+        }
+        __syncthreads();
+      }
+      if (dot) {
+        // owned columns j = warp + 8q, in batches of 8
+        for (int q0 = 0; warp + kWarps * q0 < a.ncols; q0 += 8) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int j = warp + kWarps * (q0 + u);
+            v[u] = 0.0;
+            if (j < a.ncols) {
+              const double* col = a.B + (int64_t)j * a.ldb;
+#pragma unroll
+              for (int e = 0; e < RPL; ++e) {
+                const int64_t r = r0 + lane + 32 * e;
+                if (r < s1) v[u] = fma(col[r], xv[e], v[u]);
+              }
+            }
+          }
+          const double t = warp_sum8(v);
+          const int j = warp + kWarps * (q0 + warp_sum8_index(lane));
+          if ((lane & 3) == 0 && j < a.ncols) colacc[j] += t;
+        }
+      } else if (warp == 0) {
+        double s = 0.0;
+#pragma unroll
+        for (int e = 0; e < RPL; ++e) s = fma(xv[e], xv[e], s);
+        nsum += warp_sum(s);
+      }
+    }
+    __syncthreads();
+    if (dot) {
+      for (int j = threadIdx.x; j < a.ncols; j += kThreads)
+        a.part[(int64_t)j * G + blockIdx.x] = colacc[j];
+    } else if (threadIdx.x == 0) {
+      a.part[blockIdx.x] = nsum;
+    }
+  };
+
+  if (a.ncols == 0 || a.passes == 0) {
+    sweep(false, false);
+  } else {
+    sweep(false, true);
+    for (int pass = 1; pass <= a.passes; ++pass) {
+      grid_barrier(a.bar, G);
+      coop_reduce_cols(a.part, a.ncols, (int)G, a.c);
+      grid_barrier(a.bar, G);
+      sweep(true, pass < a.passes);
+    }
+  }
+  grid_barrier(a.bar, G);
+  if (blockIdx.x == 0) {
+    // [4] norm test (k_norm_test semantics, incl. the host progress word)
+    double s = 0.0;
+    for (unsigned b = threadIdx.x; b < G; b += kThreads) s += __ldcg(a.part + b);
+    s = block_sum(s, tred[0]);
+    if (threadIdx.x == 0) nacc = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double nrm = sqrt(nacc);
+      *a.slot = nrm;
+      int stop = ST_RUNNING;
+      if (a.st->nonfinite || !isfinite(nrm)) stop = ST_NONFINITE;
+      else if (nrm < a.eps) stop = a.code;
+      if (stop != ST_RUNNING) {
+        a.st->status = stop;
+        a.st->kprime = a.step;
+        a.st->where = a.step;
+      }
+      if (a.hp && (stop != ST_RUNNING || a.side == 1)) {
+        volatile HostProg* h = a.hp;
+        if (stop != ST_RUNNING) {
+          h->status = stop;
+          h->halt_step = a.step;
+        }
+        asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(&a.hp->prog),
+                     "r"(2 * a.step + a.side)
+                     : "memory");
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tile-resident fused CGS2 (single rank): as k_cgs2_coop, but each CTA first
+// pulls its whole basis tile (rows_per_cta x ncols) from L2/HBM into shared
+// memory with one bulk-async (TMA) copy per column segment, all in flight on
+// one mbarrier, then runs every sweep of the two CGS passes out of shared
+// memory.  The basis is read from memory once per orthogonalisation instead
+// of three times, and at full bulk-copy bandwidth instead of latency-bound
+// warp loads.  Used when the tile fits in shared memory (small / medium
+// bases: the L2-resident regime where CGS is latency-bound).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+template <int MAXE>
+__global__ void __launch_bounds__(kThreads, 1)
+k_cgs2_tile(CgsCoopArgs a) {
+  if (halted(a.st)) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ double tred[kWarps][32 * MAXE];
+  __shared__ __align__(8) unsigned long long mbar;
+  __shared__ double nacc;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned G = gridDim.x;
+  const int64_t s0 = (int64_t)blockIdx.x * a.rows_per_cta;
+  const int64_t s1 = min(a.L, s0 + a.rows_per_cta);
+  const int nr = s1 > s0 ? (int)(s1 - s0) : 0;
+  const int ldt = (nr + 1) & ~1;  // 16-byte column segments
+  double* tile = reinterpret_cast<double*>(smem_raw);
+  double* cs = tile + (size_t)a.ncols * ldt;  // coefficients of the current pass
+  const uint32_t bar = smem_u32(&mbar);
+
+  // bulk-async load of the basis tile (thread 0 issues, all wait later)
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t bytes = (uint32_t)ldt * 8u;
+    const uint32_t total = bytes * (uint32_t)a.ncols;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                 "r"(total)
+                 : "memory");
+    if (bytes)
+      for (int j = 0; j < a.ncols; ++j) {
+        const double* src = a.B + (int64_t)j * a.ldb + s0;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+            "[%3];" ::"r"(smem_u32(tile + (size_t)j * ldt)),
+            "l"(src), "r"(bytes), "r"(bar)
+            : "memory");
+      }
+  }
+  // [0] finalisation of the split partial sums of A^T q (overlaps the copy)
+  if (a.fpart) {
+    for (int64_t r = s0 + threadIdx.x; r < s1; r += kThreads) {
+      double v = 0.0;
+      for (int k = 0; k < a.fnsplit; ++k) v += a.fpart[(int64_t)k * a.fld + r];
+      if (a.fp) v = v - (*a.fbeta) * a.fp[r];
+      a.x[r] = v;
+      flag_nonfinite(a.st, v, a.step);
+    }
+  }
+  unsigned long long tl = 0;
+  phase_mark(a.tdbg, 0, tl);
+  __syncthreads();
+  // x rows of this CTA live in registers for the whole kernel (loaded while
+  // the tile is in flight)
+  double xv[MAXE];
+#pragma unroll
+  for (int e = 0; e < MAXE; ++e) {
+    const int rl = lane + 32 * e;
+    xv[e] = rl < nr ? a.x[s0 + rl] : 0.0;
+  }
+  while (!mbar_try_wait(bar, 0)) {
+  }
+  phase_mark(a.tdbg, 1, tl);  // [1] bulk copy of the tile (+ finalisation)
+
+  auto sweep = [&](bool update, bool dot) {
+    if (update) {
+      for (int j = threadIdx.x; j < a.ncols; j += kThreads) cs[j] = __ldcg(a.c + j);
+      __syncthreads();
+      double t[MAXE];
+#pragma unroll
+      for (int e = 0; e < MAXE; ++e) t[e] = 0.0;
+#pragma unroll 4
+      for (int j = warp; j < a.ncols; j += kWarps) {
+        const double cj = cs[j];
+        const double* col = tile + (size_t)j * ldt;
+#pragma unroll
+        for (int e = 0; e < MAXE; ++e) {
+          const int rl = lane + 32 * e;
+          if (rl < nr) t[e] = fma(col[rl], cj, t[e]);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < MAXE; ++e) tred[warp][lane + 32 * e] = t[e];
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < MAXE; ++e) {
+        double s = tred[0][lane + 32 * e];
+#pragma unroll
+        for (int w = 1; w < kWarps; ++w) s += tred[w][lane + 32 * e];
+        xv[e] = xv[e] - s;
+        const int rl = lane + 32 * e;
+        if (!dot && warp == 0 && rl < nr) a.x[s0 + rl] = xv[e];  // final pass only
+      }
+      __syncthreads();
+    }
+    if (dot) {
+      for (int q0 = 0; warp + kWarps * q0 < a.ncols; q0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int j = warp + kWarps * (q0 + u);
+          v[u] = 0.0;
+          if (j < a.ncols) {
+            const double* col = tile + (size_t)j * ldt;
+#pragma unroll
+            for (int e = 0; e < MAXE; ++e) {
+              const int rl = lane + 32 * e;
+              if (rl < nr) v[u] = fma(col[rl], xv[e], v[u]);
+            }
+          }
+        }
+        const double t = warp_sum8(v);
+        const int j = warp + kWarps * (q0 + warp_sum8_index(lane));
+        if ((lane & 3) == 0 && j < a.ncols) a.part[(int64_t)j * G + blockIdx.x] = t;
+      }
+    } else if (warp == 0) {
+      double s = 0.0;
+#pragma unroll
+      for (int e = 0; e < MAXE; ++e) s = fma(xv[e], xv[e], s);
+      s = warp_sum(s);
+      if (lane == 0) a.part[blockIdx.x] = s;
+    }
+  };
+
+  if (a.ncols == 0 || a.passes == 0) {
+    sweep(false, false);
+    phase_mark(a.tdbg, 2, tl);
+  } else {
+    sweep(false, true);
+    phase_mark(a.tdbg, 2, tl);  // [2] sweeps
+    for (int pass = 1; pass <= a.passes; ++pass) {
+      grid_barrier(a.bar, G);
+      phase_mark(a.tdbg, 3, tl);  // [3] barriers
+      coop_reduce_cols(a.part, a.ncols, (int)G, a.c);
+      phase_mark(a.tdbg, 4, tl);  // [4] reductions
+      grid_barrier(a.bar, G);
+      phase_mark(a.tdbg, 3, tl);
+      sweep(true, pass < a.passes);
+      phase_mark(a.tdbg, 2, tl);
+    }
+  }
+  grid_barrier(a.bar, G);
+  phase_mark(a.tdbg, 3, tl);
+  if (blockIdx.x == 0) {
+    double s = 0.0;
+    for (unsigned b = threadIdx.x; b < G; b += kThreads) s += __ldcg(a.part + b);
+    s = block_sum(s, tred[0]);
+    if (threadIdx.x == 0) nacc = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double nrm = sqrt(nacc);
+      *a.slot = nrm;
+      int stop = ST_RUNNING;
+      if (a.st->nonfinite || !isfinite(nrm)) stop = ST_NONFINITE;
+      else if (nrm < a.eps) stop = a.code;
+      if (stop != ST_RUNNING) {
+        a.st->status = stop;
+        a.st->kprime = a.step;
+        a.st->where = a.step;
+      }
+      if (a.hp && (stop != ST_RUNNING || a.side == 1)) {
+        volatile HostProg* h = a.hp;
+        if (stop != ST_RUNNING) {
+          h->status = stop;
+          h->halt_step = a.step;
+        }
+        asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(&a.hp->prog),
+                     "r"(2 * a.step + a.side)
+                     : "memory");
+      }
+    }
   }
 }
 

@@ -10,10 +10,16 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <immintrin.h>
+
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -81,6 +87,11 @@ struct ksvd_ctx {
   double prof_ms[KC_NUM] = {};
   int64_t prof_n[KC_NUM] = {};
   cudaEvent_t marks[8] = {};
+  // GK-loop pacing (one loop at a time per context)
+  HostProg* hprog = nullptr;  // mapped host memory (host view)
+  HostProg* dprog = nullptr;  // device view of the same memory
+  cudaEvent_t ring_ev[8] = {};
+  unsigned long long* tdbg = nullptr;  // KSVD_PHASE_TIMES: CGS phase timing
 };
 
 static int get_event(ksvd_ctx* c, cudaEvent_t* ev) {
@@ -138,18 +149,18 @@ static int allreduce(ksvd_ctx* c, double* buf, size_t count) {
 // ---------------------------------------------------------------------------
 // matrices
 struct GemvNPlan {
-  int V, nchunks, chunk_vecs, blocks_per_chunk;
-  int64_t nvec, groups_per_warp;
-  size_t smem;
+  int V, U, nchunks;
+  int64_t nvec, rows_per_warp, blocks;
 };
 struct GemvTPlan {
   int64_t ncoltiles, nsplit, rows_per_split;
+  int rg;  // row groups per CTA (k_gemv_t RG)
 };
 
-constexpr int kRowsPerWarp = 2;  // R of k_gemv_n
-constexpr int kUnrollN = 4;      // U of k_gemv_n
-constexpr int kUnrollT = 8;      // U of k_gemv_t
-constexpr int kMaxChunkDoubles = 8192;  // 64 KB of p per CTA
+constexpr int kUnrollN64 = 4;  // U of k_gemv_n2 for f64 A (32*U 16-byte vectors / chunk)
+constexpr int kUnrollN32 = 2;  // U of k_gemv_n2 for f32 A
+constexpr int kUnrollT = 16;   // U of k_gemv_t
+constexpr int kGemvTCtasPerSm = 4;
 
 struct ksvd_mat {
   ksvd_ctx* ctx = nullptr;
@@ -168,17 +179,9 @@ struct ksvd_mat {
 
 static size_t esize(int dtype) { return dtype == KSVD_F32 ? 4 : 8; }
 
-template <typename TA>
-static int set_smem_attr(size_t smem) {
-  auto kn = k_gemv_n<TA, kRowsPerWarp, kUnrollN>;
-  CK(cudaFuncSetAttribute(kn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  return 0;
-}
-
-template <typename TA>
-static int occupancy_n(size_t smem, int* out) {
-  auto kn = k_gemv_n<TA, kRowsPerWarp, kUnrollN>;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, kn, kThreads, smem));
+template <typename TA, int U>
+static int occupancy_n2(int* out) {
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k_gemv_n2<TA, U>, kThreads, 0));
   return 0;
 }
 
@@ -187,29 +190,29 @@ static int plan_matrix(ksvd_mat* M) {
   const int64_t bytes = esize(M->dtype);
   GemvNPlan& pn = M->pn;
   pn.V = (int)(16 / bytes);
+  pn.U = M->dtype == KSVD_F32 ? kUnrollN32 : kUnrollN64;
   pn.nvec = cdiv(M->n, pn.V);
-  pn.nchunks = (int)cdiv(pn.nvec * pn.V, kMaxChunkDoubles);
-  pn.chunk_vecs = (int)cdiv(pn.nvec, pn.nchunks);
-  pn.smem = (size_t)pn.chunk_vecs * pn.V * sizeof(double);
+  pn.nchunks = (int)cdiv(pn.nvec, 32 * pn.U);
   int occ = 1;
-  if (M->dtype == KSVD_F32) {
-    TRY(set_smem_attr<float>(pn.smem));
-    TRY(occupancy_n<float>(pn.smem, &occ));
-  } else {
-    TRY(set_smem_attr<double>(pn.smem));
-    TRY(occupancy_n<double>(pn.smem, &occ));
-  }
+  if (M->dtype == KSVD_F32)
+    TRY((occupancy_n2<float, kUnrollN32>(&occ)));
+  else
+    TRY((occupancy_n2<double, kUnrollN64>(&occ)));
   occ = std::max(occ, 1);
-  const int64_t ngroups = cdiv(std::max<int64_t>(M->mloc, 1), kRowsPerWarp);
-  const int64_t warps_per_chunk =
-      std::max<int64_t>(1, (int64_t)c->sms * occ * kWarps / pn.nchunks);
-  pn.groups_per_warp = cdiv(ngroups, warps_per_chunk);
-  const int64_t warps_needed = cdiv(ngroups, pn.groups_per_warp);
-  pn.blocks_per_chunk = (int)cdiv(warps_needed, kWarps);
+  const int64_t warps = (int64_t)c->sms * occ * kWarps;
+  int64_t rsegs = std::max<int64_t>(1, warps / pn.nchunks);
+  pn.rows_per_warp = rup(cdiv(std::max<int64_t>(M->mloc, 1), rsegs), 8);
+  rsegs = cdiv(std::max<int64_t>(M->mloc, 1), pn.rows_per_warp);
+  pn.blocks = cdiv(rsegs * pn.nchunks, kWarps);
 
   GemvTPlan& pt = M->pt;
-  pt.ncoltiles = cdiv(pn.nvec, kThreads);
-  const int64_t target = (int64_t)c->sms * 8;
+  // RG row groups: narrower column tiles -> fewer row splits -> a short
+  // partial-sum finalisation (KSVD_GEMVT_RG overrides, for experiments)
+  pt.rg = 8;
+  if (const char* e = getenv("KSVD_GEMVT_RG")) pt.rg = atoi(e);
+  if (pt.rg != 1 && pt.rg != 2 && pt.rg != 4 && pt.rg != 8) pt.rg = 8;
+  pt.ncoltiles = cdiv(pn.nvec, kThreads / pt.rg);
+  const int64_t target = (int64_t)c->sms * kGemvTCtasPerSm;
   int64_t nsplit = std::max<int64_t>(1, cdiv(target, pt.ncoltiles));
   int64_t rps = std::max<int64_t>(64, cdiv(std::max<int64_t>(M->mloc, 1), nsplit));
   pt.rows_per_split = rps;
@@ -221,8 +224,7 @@ static int alloc_matrix_buffers(ksvd_mat* M) {
   const size_t abytes = (size_t)M->mloc * M->lda * esize(M->dtype);
   CK(cudaMalloc(&M->A, std::max<size_t>(abytes, 16)));
   TRY(plan_matrix(M));
-  if (M->pn.nchunks > 1)
-    CK(cudaMalloc(&M->part_n, sizeof(double) * M->pn.nchunks * std::max<int64_t>(M->mloc, 1)));
+  CK(cudaMalloc(&M->part_n, sizeof(double) * M->pn.nchunks * std::max<int64_t>(M->mloc, 1)));
   CK(cudaMalloc(&M->part_t, sizeof(double) * M->pt.nsplit * M->n_pad));
   CK(cudaMalloc(&M->dx, sizeof(double) * std::max(M->n_pad, M->m_pad)));
   CK(cudaMalloc(&M->dy, sizeof(double) * std::max(M->n_pad, M->m_pad)));
@@ -248,62 +250,70 @@ static int free_matrix(ksvd_mat* M) {
 }
 
 // w = A p (- alpha q): p_src/p_scale/p_dst per k_gemv_n; out = w (m rows)
+// w = A p (- alpha q): partial row sums per column chunk (k_gemv_n2), then
+// the chunk sums + epilogue (k_gemv_n_finalize) unless the caller fuses the
+// finalisation into its k_cgs2_* launch (finalize = false).
 static int enqueue_gemv_n(ksvd_mat* M, const double* p_src, const double* p_scale,
                           double* p_dst, const double* qprev, const double* alpha,
-                          double* w, DevState* st, int step) {
+                          double* w, DevState* st, int step, bool finalize = true) {
   ksvd_ctx* c = M->ctx;
   const GemvNPlan& pn = M->pn;
   if (M->mloc == 0) return 0;
-  const bool direct = pn.nchunks == 1;
-  dim3 grid(pn.blocks_per_chunk, pn.nchunks);
-  double* out = direct ? w : M->part_n;
-  const int64_t out_ld = direct ? 0 : M->mloc;
+  const dim3 grid((unsigned)pn.blocks);
   if (M->dtype == KSVD_F32) {
-    TRY(launch(c, KC_GEMV_N, k_gemv_n<float, kRowsPerWarp, kUnrollN>, grid,
-               dim3(kThreads), pn.smem, (const float*)M->A, M->lda, M->mloc,
-               pn.nvec, pn.chunk_vecs, p_src, p_scale, p_dst, M->n, out, out_ld,
-               direct ? qprev : (const double*)nullptr,
-               direct ? alpha : (const double*)nullptr, st, step,
-               pn.groups_per_warp));
+    TRY(launch(c, KC_GEMV_N, k_gemv_n2<float, kUnrollN32>, grid, dim3(kThreads), 0,
+               (const float*)M->A, M->lda, M->mloc, pn.nvec, pn.nchunks, pn.rows_per_warp,
+               p_src, p_scale, p_dst, M->n, M->part_n, (const DevState*)st));
   } else {
-    TRY(launch(c, KC_GEMV_N, k_gemv_n<double, kRowsPerWarp, kUnrollN>, grid,
-               dim3(kThreads), pn.smem, (const double*)M->A, M->lda, M->mloc,
-               pn.nvec, pn.chunk_vecs, p_src, p_scale, p_dst, M->n, out, out_ld,
-               direct ? qprev : (const double*)nullptr,
-               direct ? alpha : (const double*)nullptr, st, step,
-               pn.groups_per_warp));
+    TRY(launch(c, KC_GEMV_N, k_gemv_n2<double, kUnrollN64>, grid, dim3(kThreads), 0,
+               (const double*)M->A, M->lda, M->mloc, pn.nvec, pn.nchunks, pn.rows_per_warp,
+               p_src, p_scale, p_dst, M->n, M->part_n, (const DevState*)st));
   }
-  if (!direct) {
+  if (finalize)
     TRY(launch(c, KC_FIN, k_gemv_n_finalize, dim3((unsigned)cdiv(M->mloc, kThreads)),
-               dim3(kThreads), 0, (const double*)M->part_n, M->mloc, pn.nchunks,
-               M->mloc, qprev, alpha, w, st, step));
-  }
+               dim3(kThreads), 0, (const double*)M->part_n, M->mloc, pn.nchunks, M->mloc,
+               qprev, alpha, w, st, step));
   return 0;
+}
+
+template <typename TA>
+static int launch_gemv_t(ksvd_mat* M, dim3 grid, const double* q_src, const double* q_scale,
+                         double* q_dst, DevState* st) {
+  ksvd_ctx* c = M->ctx;
+  const GemvTPlan& pt = M->pt;
+#define KSVD_GT(RG)                                                                    \
+  launch(c, KC_GEMV_T, k_gemv_t<TA, kUnrollT, RG>, grid, dim3(kThreads), 0,             \
+         (const TA*)M->A, M->lda, M->mloc, M->pn.nvec, pt.rows_per_split, q_src, q_scale, \
+         q_dst, M->part_t, M->n_pad, (const DevState*)st)
+  switch (pt.rg) {
+    case 1: return KSVD_GT(1);
+    case 2: return KSVD_GT(2);
+    case 4: return KSVD_GT(4);
+    default: return KSVD_GT(8);
+  }
+#undef KSVD_GT
 }
 
 // z = sum_ranks A^T q (- beta p): q_src/q_scale/q_dst per k_gemv_t.
 static int enqueue_gemv_t(ksvd_mat* M, const double* q_src, const double* q_scale,
                           double* q_dst, const double* beta, const double* pprev,
-                          double* z, DevState* st, int step, bool check) {
+                          double* z, DevState* st, int step, bool check,
+                          bool finalize = true) {
   ksvd_ctx* c = M->ctx;
   const GemvTPlan& pt = M->pt;
   if (M->mloc > 0) {
     dim3 grid((unsigned)pt.ncoltiles, (unsigned)pt.nsplit);
-    if (M->dtype == KSVD_F32) {
-      TRY(launch(c, KC_GEMV_T, k_gemv_t<float, kUnrollT>, grid, dim3(kThreads), 0,
-                 (const float*)M->A, M->lda, M->mloc, M->pn.nvec, pt.rows_per_split,
-                 q_src, q_scale, q_dst, M->part_t, M->n_pad, (const DevState*)st));
-    } else {
-      TRY(launch(c, KC_GEMV_T, k_gemv_t<double, kUnrollT>, grid, dim3(kThreads), 0,
-                 (const double*)M->A, M->lda, M->mloc, M->pn.nvec, pt.rows_per_split,
-                 q_src, q_scale, q_dst, M->part_t, M->n_pad, (const DevState*)st));
-    }
+    if (M->dtype == KSVD_F32)
+      TRY(launch_gemv_t<float>(M, grid, q_src, q_scale, q_dst, st));
+    else
+      TRY(launch_gemv_t<double>(M, grid, q_src, q_scale, q_dst, st));
   } else {
     CK(cudaMemsetAsync(M->part_t, 0, sizeof(double) * M->n_pad, c->stream));
   }
   const int nsplit = M->mloc > 0 ? (int)pt.nsplit : 1;
   const bool multi = c->nranks > 1;
-  TRY(launch(c, KC_FIN, k_gemv_t_finalize, dim3((unsigned)cdiv(M->n_pad, kThreads)),
+  if (!finalize && !multi) return 0;  // fused into the caller's k_cgs2_coop
+  TRY(launch(c, KC_FIN, k_gemv_t_finalize, dim3((unsigned)cdiv(M->n_pad, 32)),
              dim3(kThreads), 0, (const double*)M->part_t, M->n_pad, nsplit, M->n,
              M->n_pad, multi ? (const double*)nullptr : beta,
              multi ? (const double*)nullptr : pprev, z, st, step,
@@ -323,73 +333,212 @@ struct CgsWork {
   double* part = nullptr;  // nrb x cap
   double* c = nullptr;     // cap
   double* red = nullptr;   // 2
+  unsigned* bar = nullptr; // grid barrier {count, generation}
   int64_t part_elems = 0;
   int cap = 0;
 };
 
-static int choose_E(const ksvd_ctx* c, int64_t L) {
-  if (L >= (int64_t)kThreads * 4 * c->sms * 2) return 4;
-  if (L >= (int64_t)kThreads * 2 * c->sms) return 2;
+static int choose_rpl(int64_t L) {
+  // rows per lane of k_cgs_rows: keep >= ~600 row blocks for parallelism,
+  // but fewer, fatter blocks for long vectors (shorter partial reductions)
+  if (L >= 128 * 600) return 4;
+  if (L >= 64 * 600) return 2;
   return 1;
 }
 
-static int ensure_cgs(CgsWork* w, int64_t nrb, int cols) {
+// Grow-only, geometric, stream-ordered (cudaFree would synchronise the
+// device inside the GK loop).
+static int ensure_cgs(cudaStream_t s, CgsWork* w, int64_t nrb, int cols) {
   const int64_t need = nrb * std::max(cols, 1);
   if (need > w->part_elems) {
-    cudaFree(w->part);
-    CK(cudaMalloc(&w->part, sizeof(double) * need));
-    w->part_elems = need;
+    const int64_t n = std::max(need, 2 * w->part_elems);
+    if (w->part) CK(cudaFreeAsync(w->part, s));
+    CK(cudaMallocAsync(&w->part, sizeof(double) * n, s));
+    w->part_elems = n;
   }
   if (cols > w->cap || !w->c) {
-    cudaFree(w->c);
-    w->cap = std::max(cols, 64);
-    CK(cudaMalloc(&w->c, sizeof(double) * w->cap));
+    const int n = std::max(std::max(cols, 64), 2 * w->cap);
+    if (w->c) CK(cudaFreeAsync(w->c, s));
+    CK(cudaMallocAsync(&w->c, sizeof(double) * n, s));
+    w->cap = n;
   }
-  if (!w->red) CK(cudaMalloc(&w->red, sizeof(double) * 4));
+  if (!w->red) CK(cudaMallocAsync(&w->red, sizeof(double) * 4, s));
+  if (!w->bar) {
+    CK(cudaMallocAsync((void**)&w->bar, sizeof(unsigned) * 2, s));
+    CK(cudaMemsetAsync(w->bar, 0, sizeof(unsigned) * 2, s));
+  }
   return 0;
 }
 
-template <int E>
+template <int RPL>
 static int cgs_impl(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int ncols,
                     double* x, int64_t L, int passes, bool sharded, double eps,
-                    double* slot, DevState* st, int step, int code) {
-  const int64_t nrb = std::max<int64_t>(1, cdiv(L, (int64_t)kThreads * E));
-  TRY(ensure_cgs(W, nrb, ncols));
+                    double* slot, DevState* st, int step, int code, HostProg* hp,
+                    int side) {
+  const int64_t nrb = std::max<int64_t>(1, cdiv(L, 32 * RPL));
+  TRY(ensure_cgs(c->stream, W, nrb, ncols));
   const bool multi = sharded && c->nranks > 1;
   double* part = W->part;
-  const unsigned rgrid = (unsigned)cdiv(std::max(ncols, 1), kWarps);
+  const dim3 grid((unsigned)nrb), block(kThreads);
+  auto rows = k_cgs_rows<RPL>;
   if (ncols == 0) {
-    TRY(launch(c, KC_CGS, k_sumsq<E>, dim3((unsigned)nrb), dim3(kThreads), 0,
-               (const double*)x, L, part, (const DevState*)st));
+    TRY(launch(c, KC_CGS, rows, grid, block, 0, B, ldb, 0, (const double*)nullptr, x, L,
+               kNorm, part, (int)nrb, (const DevState*)st));
   } else {
-    TRY(launch(c, KC_CGS, k_cgs_dot<E>, dim3((unsigned)nrb, (unsigned)cdiv(ncols, kJ)),
-               dim3(kThreads), 0, B, ldb, ncols, (const double*)x, L, part, (int)nrb,
-               (const DevState*)st));
-    TRY(launch(c, KC_CGS, k_reduce_cols, dim3(rgrid), dim3(kThreads), 0,
-               (const double*)part, (int)nrb, ncols, W->c, (const DevState*)st));
-    if (multi) TRY(allreduce(c, W->c, ncols));
+    // pass 1 coefficients
+    TRY(launch(c, KC_CGS, rows, grid, block, 0, B, ldb, ncols, (const double*)nullptr, x, L,
+               kDot, part, (int)nrb, (const DevState*)st));
     for (int pass = 1; pass <= passes; ++pass) {
-      const int mode = pass < passes ? 1 : 2;
-      TRY(launch(c, KC_CGS, k_cgs_update<E>, dim3((unsigned)nrb), dim3(kThreads), 0, B,
-                 ldb, ncols, (const double*)W->c, x, L, mode, part, (int)nrb,
-                 (const DevState*)st));
-      if (mode == 1) {
-        TRY(launch(c, KC_CGS, k_reduce_cols, dim3(rgrid), dim3(kThreads), 0,
-                   (const double*)part, (int)nrb, ncols, W->c, (const DevState*)st));
-        if (multi) TRY(allreduce(c, W->c, ncols));
-      }
+      TRY(launch(c, KC_CGS, k_reduce_part, dim3((unsigned)ncols), block, 0,
+                 (const double*)part, (int)nrb, W->c, (const DevState*)st));
+      if (multi) TRY(allreduce(c, W->c, ncols));
+      // update, fused with the next pass's coefficients or the final norm
+      const int mode = kUpdate | (pass < passes ? kDot : kNorm);
+      TRY(launch(c, KC_CGS, rows, grid, block, 0, B, ldb, ncols, (const double*)W->c, x, L,
+                 mode, part, (int)nrb, (const DevState*)st));
     }
   }
   if (multi) {
-    TRY(launch(c, KC_CGS, k_norm_prep, dim3(1), dim3(32), 0, (const double*)part,
-               (int)nrb, W->red, (const DevState*)st));
+    TRY(launch(c, KC_CGS, k_norm_prep, dim3(1), block, 0, (const double*)part, (int)nrb,
+               W->red, (const DevState*)st));
     TRY(allreduce(c, W->red, 2));
-    TRY(launch(c, KC_CGS, k_norm_test, dim3(1), dim3(32), 0, (const double*)nullptr, 0,
-               (const double*)W->red, eps, slot, st, step, code));
+    TRY(launch(c, KC_CGS, k_norm_test, dim3(1), block, 0, (const double*)nullptr, 0,
+               (const double*)W->red, eps, slot, st, step, code, hp, side));
   } else {
-    TRY(launch(c, KC_CGS, k_norm_test, dim3(1), dim3(32), 0, (const double*)part,
-               (int)nrb, (const double*)nullptr, eps, slot, st, step, code));
+    TRY(launch(c, KC_CGS, k_norm_test, dim3(1), block, 0, (const double*)part, (int)nrb,
+               (const double*)nullptr, eps, slot, st, step, code, hp, side));
   }
+  return 0;
+}
+
+// ---- single-rank fused CGS2 (k_cgs2_coop) ----
+constexpr int kCoopRPL = 4;
+constexpr int kCoopMaxCols = 12288;  // colacc in dynamic shared memory (96 KB)
+
+struct FinArgs {  // deferred gemv_t finalisation (phase 0 of k_cgs2_coop)
+  const double* part = nullptr;
+  int64_t ld = 0;
+  int nsplit = 0;
+  const double* beta = nullptr;
+  const double* p = nullptr;
+};
+
+static bool coop_enabled(const ksvd_ctx* c, int ncols) {
+  static const bool off = [] {
+    const char* e = getenv("KSVD_COOP");
+    return e && strcmp(e, "0") == 0;
+  }();
+  return !off && c->nranks == 1 && ncols <= kCoopMaxCols;
+}
+
+static int coop_max_ctas(ksvd_ctx* c) {
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    auto k = k_cgs2_coop<kCoopRPL>;
+    const int smem = kCoopMaxCols * (int)sizeof(double);
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, smem));
+    per_sm = std::max(1, std::min(occ, 2));
+  }
+  return per_sm * c->sms;
+}
+
+constexpr size_t kTileSmemMax = 200 * 1024;  // basis tile budget of k_cgs2_tile
+
+template <int MAXE>
+static int tile_attr() {
+  static bool done = false;
+  if (!done) {
+    CK(cudaFuncSetAttribute(k_cgs2_tile<MAXE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kTileSmemMax));
+    done = true;
+  }
+  return 0;
+}
+
+static int cgs_coop(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int ncols, double* x,
+                    int64_t L, int passes, double eps, double* slot, DevState* st, int step,
+                    int code, HostProg* hp, int side, const FinArgs& fin) {
+  CgsCoopArgs a{};
+  a.B = B;
+  a.ldb = ldb;
+  a.ncols = ncols;
+  a.x = x;
+  a.L = L;
+  a.passes = ncols > 0 ? passes : 0;
+  a.eps = eps;
+  a.slot = slot;
+  a.st = st;
+  a.step = step;
+  a.code = code;
+  a.hp = hp;
+  a.side = side;
+  a.fpart = fin.part;
+  a.fld = fin.ld;
+  a.fnsplit = fin.nsplit;
+  a.fbeta = fin.beta;
+  a.fp = fin.p;
+  a.tdbg = c->tdbg;
+  void* args[] = {&a};
+
+  // tile-resident variant: one CTA per SM, each CTA's basis tile in smem
+  int64_t G = std::min<int64_t>(c->sms, std::max<int64_t>(1, cdiv(L, 32)));
+  int64_t rows = rup(cdiv(std::max<int64_t>(L, 1), G), 2);
+  G = std::max<int64_t>(1, cdiv(L, rows));
+  const size_t tile_bytes = sizeof(double) * (size_t)ncols * (size_t)(rows + 1);
+  const void* kern = nullptr;
+  size_t smem = 0;
+  static const bool tile_off = [] {
+    const char* e = getenv("KSVD_TILE");
+    return e && strcmp(e, "0") == 0;
+  }();
+  if (!tile_off && rows <= 256 && tile_bytes <= kTileSmemMax) {
+    smem = std::max<size_t>(tile_bytes, 16);
+    switch ((int)cdiv(rows, 32)) {
+#define KSVD_TILE_CASE(E)                     \
+  case E:                                     \
+    TRY(tile_attr<E>());                      \
+    kern = (const void*)k_cgs2_tile<E>;       \
+    break;
+      KSVD_TILE_CASE(1)
+      KSVD_TILE_CASE(2)
+      KSVD_TILE_CASE(3)
+      KSVD_TILE_CASE(4)
+      KSVD_TILE_CASE(5)
+      KSVD_TILE_CASE(6)
+      KSVD_TILE_CASE(7)
+      default:
+        TRY(tile_attr<8>());
+        kern = (const void*)k_cgs2_tile<8>;
+#undef KSVD_TILE_CASE
+    }
+  } else {
+    constexpr int CH = 32 * kCoopRPL;
+    G = std::min<int64_t>(coop_max_ctas(c), std::max<int64_t>(1, cdiv(L, CH)));
+    rows = rup(cdiv(std::max<int64_t>(L, 1), G), 32);
+    G = std::max<int64_t>(1, cdiv(L, rows));
+    smem = sizeof(double) * std::max(ncols, 1);
+    kern = (const void*)k_cgs2_coop<kCoopRPL>;
+  }
+  a.rows_per_cta = (int)rows;
+  TRY(ensure_cgs(c->stream, W, G, ncols));
+  a.part = W->part;
+  a.c = W->c;
+  a.bar = W->bar;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->profiling) {
+    TRY(get_event(c, &e0));
+    TRY(get_event(c, &e1));
+    CK(cudaEventRecord(e0, c->stream));
+  }
+  CK(cudaLaunchCooperativeKernel(kern, dim3((unsigned)G), dim3(kThreads), args, smem,
+                                 c->stream));
+  if (c->profiling) {
+    CK(cudaEventRecord(e1, c->stream));
+    c->pending.push_back({e0, e1, KC_CGS});
+  }
+  c->launches++;
   return 0;
 }
 
@@ -397,21 +546,25 @@ static int cgs_impl(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int n
 // ||x|| < eps sets status `code` at `step`.
 static int cgs(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int ncols,
                double* x, int64_t L, int passes, bool sharded, double eps,
-               double* slot, DevState* st, int step, int code) {
-  switch (choose_E(c, L)) {
+               double* slot, DevState* st, int step, int code, HostProg* hp = nullptr,
+               int side = 0) {
+  switch (choose_rpl(L)) {
     case 4:
-      return cgs_impl<4>(c, W, B, ldb, ncols, x, L, passes, sharded, eps, slot, st, step, code);
+      return cgs_impl<4>(c, W, B, ldb, ncols, x, L, passes, sharded, eps, slot, st, step, code,
+                         hp, side);
     case 2:
-      return cgs_impl<2>(c, W, B, ldb, ncols, x, L, passes, sharded, eps, slot, st, step, code);
+      return cgs_impl<2>(c, W, B, ldb, ncols, x, L, passes, sharded, eps, slot, st, step, code,
+                         hp, side);
     default:
-      return cgs_impl<1>(c, W, B, ldb, ncols, x, L, passes, sharded, eps, slot, st, step, code);
+      return cgs_impl<1>(c, W, B, ldb, ncols, x, L, passes, sharded, eps, slot, st, step, code,
+                         hp, side);
   }
 }
 
 // ---------------------------------------------------------------------------
 // runs
-constexpr int kLag = 3;   // steps enqueued ahead of the last checked status
-constexpr int kRing = 8;  // pinned status ring
+constexpr int kLag = 3;   // steps enqueued ahead of the last completed one
+constexpr int kRing = 8;  // event ring (kRing > kLag)
 
 struct ksvd_run {
   ksvd_mat* M = nullptr;
@@ -428,8 +581,6 @@ struct ksvd_run {
   int kprime = 0, flags = 0, status = 0;
   // Ritz
   double *G = nullptr, *V = nullptr, *U = nullptr, *sig = nullptr;
-  int* h_ring = nullptr;
-  cudaEvent_t ring_ev[kRing] = {};
 };
 
 static int grow_bases(ksvd_run* R, int need_cols) {
@@ -461,16 +612,13 @@ static void free_run(ksvd_run* R) {
   if (!R) return;
   ksvd_ctx* c = R->M->ctx;
   cudaSetDevice(c->device);
-  cudaStreamSynchronize(c->stream);
-  for (double* p : {R->Q, R->P, R->w, R->z, R->alpha, R->beta, R->slot, R->G, R->V,
-                    R->U, R->sig, R->left.part, R->left.c, R->left.red, R->right.part,
-                    R->right.c, R->right.red})
-    cudaFree(p);
-  cudaFree(R->st);
-  cudaFree(R->st_aux);
-  for (auto& e : R->ring_ev)
-    if (e) cudaEventDestroy(e);
-  if (R->h_ring) cudaFreeHost(R->h_ring);
+  // stream-ordered frees back to the (non-trimming) pool: no device sync
+  for (void* p : {(void*)R->Q, (void*)R->P, (void*)R->w, (void*)R->z, (void*)R->alpha,
+                  (void*)R->beta, (void*)R->slot, (void*)R->G, (void*)R->V, (void*)R->U,
+                  (void*)R->sig, (void*)R->left.part, (void*)R->left.c, (void*)R->left.red,
+                  (void*)R->left.bar, (void*)R->right.part, (void*)R->right.c,
+                  (void*)R->right.red, (void*)R->right.bar, (void*)R->st, (void*)R->st_aux})
+    if (p) cudaFreeAsync(p, c->stream);
   delete R;
 }
 
@@ -484,10 +632,17 @@ static int enqueue_step(ksvd_run* R, int i) {
   TRY(grow_bases(R, i + 1 <= R->k_max ? i + 1 : i));
   // w = A p_i - alpha_i q_i, with p_i = z / alpha_i stored to P[:, i-1]
   TRY(enqueue_gemv_n(M, R->z, R->alpha + i, Pcol(R, i - 1), Qcol(R, i - 1), R->alpha + i,
-                     R->w, R->st, i));
+                     R->w, R->st, i, /*finalize=*/!coop_enabled(c, i)));
   // CGS2 against Q[:, :i]; beta_{i+1} = ||w||; beta < eps -> breakdown
-  TRY(cgs(c, &R->left, R->Q, R->ldq, i, R->w, M->mloc, R->reorth, true, R->eps,
-          R->beta + i + 1, R->st, i, ST_BETA_BREAK));
+  if (coop_enabled(c, i)) {
+    FinArgs fin{M->part_n, M->mloc, M->mloc > 0 ? M->pn.nchunks : 0, R->alpha + i,
+                Qcol(R, i - 1)};
+    TRY(cgs_coop(c, &R->left, R->Q, R->ldq, i, R->w, M->mloc, R->reorth, R->eps,
+                 R->beta + i + 1, R->st, i, ST_BETA_BREAK, R->M->ctx->dprog, 0, fin));
+  } else {
+    TRY(cgs(c, &R->left, R->Q, R->ldq, i, R->w, M->mloc, R->reorth, true, R->eps,
+            R->beta + i + 1, R->st, i, ST_BETA_BREAK, R->M->ctx->dprog, 0));
+  }
   if (i == R->k_max) {
     // q_{k+1} = w / beta; stop before alpha_{k+1} (bidiag.py:165-168)
     TRY(launch(c, KC_OTHER, k_scale, dim3((unsigned)cdiv(std::max<int64_t>(M->mloc, 1), kThreads)),
@@ -495,12 +650,21 @@ static int enqueue_step(ksvd_run* R, int i) {
                Qcol(R, i), M->mloc, (const DevState*)R->st));
     return 0;
   }
-  // z = A^T q_{i+1} - beta_{i+1} p_i, q_{i+1} = w / beta stored to Q[:, i]
-  TRY(enqueue_gemv_t(M, R->w, R->beta + i + 1, Qcol(R, i), R->beta + i + 1, Pcol(R, i - 1),
-                     R->z, R->st, i, true));
-  // CGS2 against P[:, :i] (replicated, no collective); alpha_{i+1} = ||z||
-  TRY(cgs(c, &R->right, R->P, R->ldp, i, R->z, M->n, R->reorth, false, R->eps,
-          R->alpha + i + 1, R->st, i, ST_ALPHA_BREAK));
+  // z = A^T q_{i+1} - beta_{i+1} p_i, q_{i+1} = w / beta stored to Q[:, i];
+  // then CGS2 against P[:, :i] (replicated, no collective); alpha_{i+1} = ||z||
+  if (coop_enabled(c, i)) {
+    TRY(enqueue_gemv_t(M, R->w, R->beta + i + 1, Qcol(R, i), R->beta + i + 1, Pcol(R, i - 1),
+                       R->z, R->st, i, true, /*finalize=*/false));
+    FinArgs fin{M->part_t, M->n_pad, M->mloc > 0 ? (int)M->pt.nsplit : 0, R->beta + i + 1,
+                Pcol(R, i - 1)};
+    TRY(cgs_coop(c, &R->right, R->P, R->ldp, i, R->z, M->n, R->reorth, R->eps,
+                 R->alpha + i + 1, R->st, i, ST_ALPHA_BREAK, R->M->ctx->dprog, 1, fin));
+  } else {
+    TRY(enqueue_gemv_t(M, R->w, R->beta + i + 1, Qcol(R, i), R->beta + i + 1, Pcol(R, i - 1),
+                       R->z, R->st, i, true));
+    TRY(cgs(c, &R->right, R->P, R->ldp, i, R->z, M->n, R->reorth, false, R->eps,
+            R->alpha + i + 1, R->st, i, ST_ALPHA_BREAK, R->M->ctx->dprog, 1));
+  }
   return 0;
 }
 
@@ -546,19 +710,66 @@ static int run_loop(ksvd_run* R, const double* q1_local) {
   // z = A^T q_1; alpha_1 = ||z||; alpha_1 < eps -> degenerate (bidiag.py:139-145)
   TRY(enqueue_gemv_t(M, R->Q, nullptr, nullptr, nullptr, nullptr, R->z, R->st, 0, true));
   TRY(cgs(c, &R->right, R->P, R->ldp, 0, R->z, M->n, 0, false, R->eps, R->alpha + 1, R->st,
-          0, ST_DEGENERATE));
+          0, ST_DEGENERATE, R->M->ctx->dprog, 1));
+  // Pacing: the host enqueues step i only once step i-kLag has finished.
+  // KSVD_PACE=spin polls the mapped progress word; the default waits on a
+  // ring of events (which also flushes the launch queue).  Either way the
+  // stop decision is "the run halted at a step <= i-kLag", which depends only
+  // on values identical on every rank, so all ranks enqueue the same steps.
+  static const bool spin_mode = [] {
+    const char* e = getenv("KSVD_PACE");
+    return e && strcmp(e, "spin") == 0;
+  }();
+  static const bool dbg = getenv("KSVD_DEBUG_HOST") != nullptr;
+  using clk = std::chrono::steady_clock;
+  double t_launch = 0, t_wait = 0;
   for (int i = 1; i <= R->k_max; ++i) {
+    auto t0 = clk::now();
     if (i > kLag) {
-      const int s = (i - kLag) % kRing;
-      CK(cudaEventSynchronize(R->ring_ev[s]));
-      if (R->h_ring[s] != ST_RUNNING) break;
+      const int s = i - kLag;
+      if (spin_mode) {
+        for (int spin = 0;; ++spin) {
+          const int prog = *(volatile int*)&c->hprog->prog;
+          std::atomic_thread_fence(std::memory_order_acquire);
+          if (*(volatile int*)&c->hprog->halt_step <= s || prog >= 2 * s + 1) break;
+          if ((spin & 1023) == 1023) {
+            const cudaError_t q = cudaStreamQuery(c->stream);
+            if (q != cudaSuccess && q != cudaErrorNotReady)
+              return set_err(KSVD_ERUNTIME, "GK loop: %s", cudaGetErrorString(q));
+          }
+          _mm_pause();
+        }
+      } else {
+        CK(cudaEventSynchronize(c->ring_ev[s % kRing]));
+      }
+      std::atomic_thread_fence(std::memory_order_acquire);
+      if (*(volatile int*)&c->hprog->halt_step <= s) break;
     }
+    auto t1 = clk::now();
     TRY(enqueue_step(R, i));
-    const int s = i % kRing;
-    CK(cudaMemcpyAsync(R->h_ring + s, &R->st->status, sizeof(int), cudaMemcpyDeviceToHost,
-                       c->stream));
-    CK(cudaEventRecord(R->ring_ev[s], c->stream));
+    if (spin_mode) {
+      const cudaError_t q = cudaStreamQuery(c->stream);  // flush the launch queue
+      if (q != cudaSuccess && q != cudaErrorNotReady)
+        return set_err(KSVD_ERUNTIME, "GK loop: %s", cudaGetErrorString(q));
+    } else {
+      CK(cudaEventRecord(c->ring_ev[i % kRing], c->stream));
+    }
+    auto t2 = clk::now();
+    t_wait += std::chrono::duration<double, std::milli>(t1 - t0).count();
+    t_launch += std::chrono::duration<double, std::milli>(t2 - t1).count();
   }
+  if (c->tdbg) {
+    unsigned long long t[8];
+    CK(cudaMemcpyAsync(t, c->tdbg, sizeof t, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    fprintf(stderr, "[ksvd] cgs phases (us, CTA 0, cumulative): copy %.1f sweeps %.1f "
+            "barriers %.1f reductions %.1f\n", t[1] * 1e-3, t[2] * 1e-3, t[3] * 1e-3,
+            t[4] * 1e-3);
+    CK(cudaMemsetAsync(c->tdbg, 0, sizeof t, c->stream));
+  }
+  if (dbg)
+    fprintf(stderr, "[ksvd] gk host: %d steps, enqueue %.3f ms, wait %.3f ms, launches %lld\n",
+            R->k_max, t_launch, t_wait, (long long)c->launches);
   return read_state(R);
 }
 
@@ -611,6 +822,21 @@ int ksvd_ctx_create(int device, int rank, int nranks, const char* uid, ksvd_ctx*
   c->sms = prop.multiProcessorCount;
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   for (auto& e : c->marks) CK(cudaEventCreate(&e));
+  for (auto& e : c->ring_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CK(cudaHostAlloc((void**)&c->hprog, sizeof(HostProg), cudaHostAllocMapped));
+  if (getenv("KSVD_PHASE_TIMES")) {
+    CK(cudaMalloc((void**)&c->tdbg, 64));
+    CK(cudaMemset(c->tdbg, 0, 64));
+  }
+  CK(cudaHostGetDevicePointer((void**)&c->dprog, c->hprog, 0));
+  {
+    // keep freed pool memory mapped: per-call allocations are then cheap and
+    // synchronisation points never trigger unmapping
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  }
   if (nranks > 1) {
     ncclUniqueId id;
     memcpy(&id, uid, sizeof id);
@@ -631,6 +857,8 @@ int ksvd_ctx_destroy(ksvd_ctx* c) {
   }
   for (auto e : c->pool) cudaEventDestroy(e);
   for (auto e : c->marks) cudaEventDestroy(e);
+  for (auto e : c->ring_ev) cudaEventDestroy(e);
+  if (c->hprog) cudaFreeHost(c->hprog);
   cudaStreamDestroy(c->stream);
   delete c;
   return 0;
@@ -849,21 +1077,23 @@ int ksvd_gk_run(ksvd_mat* M, int k_max, double eps, int reorth, const double* q1
     if (e != cudaSuccess)                                                     \
       return fail(set_err(KSVD_ERUNTIME, "%s: %s", #x, cudaGetErrorString(e))); \
   } while (0)
-  RUN_CK(cudaMalloc(&R->w, sizeof(double) * R->ldq));
-  RUN_CK(cudaMalloc(&R->z, sizeof(double) * R->ldp));
+  cudaStream_t st_ = c->stream;
+  RUN_CK(cudaMallocAsync(&R->w, sizeof(double) * R->ldq, st_));
+  RUN_CK(cudaMallocAsync(&R->z, sizeof(double) * R->ldp, st_));
   RUN_CK(cudaMemsetAsync(R->w, 0, sizeof(double) * R->ldq, c->stream));
   RUN_CK(cudaMemsetAsync(R->z, 0, sizeof(double) * R->ldp, c->stream));
-  RUN_CK(cudaMalloc(&R->alpha, sizeof(double) * (k_max + 2)));
-  RUN_CK(cudaMalloc(&R->beta, sizeof(double) * (k_max + 3)));
+  RUN_CK(cudaMallocAsync(&R->alpha, sizeof(double) * (k_max + 2), st_));
+  RUN_CK(cudaMallocAsync(&R->beta, sizeof(double) * (k_max + 3), st_));
   RUN_CK(cudaMemsetAsync(R->alpha, 0, sizeof(double) * (k_max + 2), c->stream));
   RUN_CK(cudaMemsetAsync(R->beta, 0, sizeof(double) * (k_max + 3), c->stream));
-  RUN_CK(cudaMalloc(&R->slot, sizeof(double) * 8));
-  RUN_CK(cudaMalloc(&R->st, sizeof(DevState)));
-  RUN_CK(cudaMalloc(&R->st_aux, sizeof(DevState)));
+  RUN_CK(cudaMallocAsync(&R->slot, sizeof(double) * 8, st_));
+  RUN_CK(cudaMallocAsync((void**)&R->st, sizeof(DevState), st_));
+  RUN_CK(cudaMallocAsync((void**)&R->st_aux, sizeof(DevState), st_));
   RUN_CK(cudaMemsetAsync(R->st, 0, sizeof(DevState), c->stream));
   RUN_CK(cudaMemsetAsync(R->st_aux, 0, sizeof(DevState), c->stream));
-  RUN_CK(cudaMallocHost(&R->h_ring, sizeof(int) * kRing));
-  for (auto& ev : R->ring_ev) RUN_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  c->hprog->prog = -1;
+  c->hprog->halt_step = INT_MAX;
+  c->hprog->status = 0;
 #undef RUN_CK
   int rc = run_loop(R, q1_local);
   if (rc) return fail(rc);
@@ -950,15 +1180,13 @@ int ksvd_ritz(ksvd_run* R, const double* G, const double* sigma, int take, int o
   *n_good = 0;
   if (take == 0) return 0;
   const int64_t ldu = M->m_pad, ldv = M->n_pad;
-  cudaFree(R->G);
-  cudaFree(R->V);
-  cudaFree(R->U);
-  cudaFree(R->sig);
+  for (double* p : {R->G, R->V, R->U, R->sig})
+    if (p) cudaFreeAsync(p, c->stream);
   R->G = R->V = R->U = R->sig = nullptr;
-  CK(cudaMalloc(&R->G, sizeof(double) * kp * take));
-  CK(cudaMalloc(&R->V, sizeof(double) * ldv * take));
-  CK(cudaMalloc(&R->U, sizeof(double) * ldu * take));
-  CK(cudaMalloc(&R->sig, sizeof(double) * take));
+  CK(cudaMallocAsync(&R->G, sizeof(double) * kp * take, c->stream));
+  CK(cudaMallocAsync(&R->V, sizeof(double) * ldv * take, c->stream));
+  CK(cudaMallocAsync(&R->U, sizeof(double) * ldu * take, c->stream));
+  CK(cudaMallocAsync(&R->sig, sizeof(double) * take, c->stream));
   CK(cudaMemsetAsync(R->V, 0, sizeof(double) * ldv * take, c->stream));
   CK(cudaMemsetAsync(R->U, 0, sizeof(double) * ldu * take, c->stream));
   CK(cudaMemcpyAsync(R->G, G, sizeof(double) * kp * take, cudaMemcpyHostToDevice, c->stream));

@@ -251,3 +251,45 @@ def test_device_matrix_reuse_and_torch_input():
     t = torch.from_numpy(A).cuda()
     r_t = K.estimate_rank(t)
     assert r_t.rank == 30 and np.array_equal(r_t.eigenvalues, r_dev.eigenvalues)
+
+
+# ---------------------------------------------------------------- CGS paths
+_PATH_SCRIPT = r"""
+import sys, json
+sys.path.insert(0, {root!r})
+import numpy as np
+import paper_2104_10785_b200 as K
+from oracle import krylov_oracle as O
+from paper_2104_10785_b200 import synth
+out = []
+for (m, n, l, k, seed) in [(300, 200, 40, 60, 6), (2000, 700, 120, 200, 3), (5000, 1200, 300, 400, 9)]:
+    A = synth.low_rank_synth(m, n, l, seed=seed)
+    ps = K.fsvd(A, k=k, r=min(l, 30), cfg=K.BidiagConfig(k_max=k, seed=seed))
+    ref = O.fsvd_oracle(A, k, min(l, 30), seed=seed)
+    rel = float(np.max(np.abs(ps.sigma - ref.sigma) / ref.sigma))
+    cos = float(min(np.min(np.abs(np.einsum("ij,ij->j", ps.U, ref.U))),
+                    np.min(np.abs(np.einsum("ij,ij->j", ps.V, ref.V)))))
+    # relative threshold: absolute 1e-8 sits at the rounding level of the
+    # post-rank Ritz values for these spectra (see tools/diag_paths.py)
+    rep = K.estimate_rank(A, eps=1e-6, mode="relative", cfg=K.BidiagConfig(k_max=1, seed=seed))
+    out.append([rel, cos, rep.rank, l])
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("env", [{"KSVD_TILE": "0"}, {"KSVD_COOP": "0"}, {}])
+def test_cgs_paths_agree(env):
+    """The tile-resident, global-load cooperative and multi-kernel CGS2
+    paths (selected at load time) all meet the parity bar."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parent.parent)
+    res = subprocess.run([sys.executable, "-c", _PATH_SCRIPT.format(root=root)],
+                         env={**os.environ, **env}, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    for rel, cos, rank, l in json.loads(res.stdout.strip().splitlines()[-1]):
+        assert rel <= SIG_RTOL_F64 and cos >= 1 - COS_TOL_F64 and rank == l, (env, rel, cos, rank)
