@@ -148,12 +148,43 @@ int ksvd_ritz(ksvd_run *run, const double *G, const double *sigma, int take,
               int orthonormalize_u, double *U, double *V, int *n_good);
 int ksvd_run_free(ksvd_run *run);
 
+/* ---- synthetic matrices (BASELINE.json configs 3-5) -----------------------
+ * A = P diag(s) Q^T + noise * G generated in HBM (no host copy): P (m x r),
+ * Q (n x r) orthonormal (CholeskyQR2 of counter-based Gaussians), G iid
+ * N(0,1) from Philox4x32-10 keyed by (seed, global index).  Entry arithmetic
+ * is fixed by include/ksvd_gen.h so the host oracle regenerates the same
+ * rows from the factors (ksvd_matrix_gen_factors).  Each rank generates its
+ * row shard [row0, row0 + m_local) with row0 / m_local given by the
+ * balanced contiguous partition (linops.row_partition). */
+#define KSVD_SPEC_HARMONIC 0 /* s_i = s0 / i                         */
+#define KSVD_SPEC_EXP 1      /* s_i = s0 * exp(-i / p)               */
+#define KSVD_SPEC_GEOM 2     /* s_i = s0 * 10^(-p (i-1) / (r-1))     */
+typedef struct ksvd_gen_spec {
+  int64_t m, n;
+  int32_t rank;
+  int32_t dtype; /* KSVD_F64 / KSVD_F32 storage */
+  uint64_t seed;
+  int32_t spectrum;
+  int32_t pad;
+  double s0, p;
+  double noise;
+} ksvd_gen_spec;
+int ksvd_matrix_generate(ksvd_ctx *ctx, const ksvd_gen_spec *spec, ksvd_mat **out);
+/* Ps_local = P diag(s) for the local rows (m_local x r row-major), Q (n x r
+ * row-major); r receives the rank.  Either pointer may be NULL. */
+int ksvd_matrix_gen_factors(ksvd_mat *mat, double *Ps_local, double *Q, int *r);
+
 /* ---- host spectral stage ------------------------------------------------
  * All eigenpairs of the symmetric tridiagonal (d, e), descending
  * (fsvd.py:63-134, implicit-shift QL, deflation |e| <= eps(|d_m|+|d_m+1|),
  * 64 sweeps max).  G: n x n column-major or NULL when vectors == 0. */
 int ksvd_symtridiag_eig(int n, const double *d, const double *e, int vectors,
                         double *theta, double *G);
+/* theta (descending) = squared singular values of the (k+1) x k lower
+ * bidiagonal B (alphas[0..k-1], betas[1..k]) = eigenvalues of B^T B, each to
+ * high relative accuracy (bisection on the Golub-Kahan tridiagonal); the
+ * rank estimator's "tiny bidiagonal SVD" (rank.py:64). */
+int ksvd_bidiag_sv2(int k, const double *alphas, const double *betas, double *theta);
 
 #ifdef __cplusplus
 }

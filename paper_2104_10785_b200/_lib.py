@@ -31,6 +31,16 @@ _pi64 = C.POINTER(C.c_int64)
 _pd = C.POINTER(C.c_double)
 _pi = C.POINTER(C.c_int)
 
+class GenSpec(C.Structure):
+    """ksvd_gen_spec (include/ksvd.h)."""
+
+    _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("rank", C.c_int32), ("dtype", C.c_int32),
+                ("seed", C.c_uint64), ("spectrum", C.c_int32), ("pad", C.c_int32),
+                ("s0", C.c_double), ("p", C.c_double), ("noise", C.c_double)]
+
+
+SPEC_HARMONIC, SPEC_EXP, SPEC_GEOM = 0, 1, 2
+
 # name -> (restype, argtypes); mirrors include/ksvd.h one to one
 SIGNATURES = {
     "ksvd_last_error": (C.c_char_p, []),
@@ -63,6 +73,9 @@ SIGNATURES = {
     "ksvd_ritz": (C.c_int, [_vp, _pd, _pd, C.c_int, C.c_int, _pd, _pd, _pi]),
     "ksvd_run_free": (C.c_int, [_vp]),
     "ksvd_symtridiag_eig": (C.c_int, [C.c_int, _pd, _pd, C.c_int, _pd, _pd]),
+    "ksvd_bidiag_sv2": (C.c_int, [C.c_int, _pd, _pd, _pd]),
+    "ksvd_matrix_generate": (C.c_int, [_vp, C.POINTER(GenSpec), C.POINTER(_vp)]),
+    "ksvd_matrix_gen_factors": (C.c_int, [_vp, _pd, _pd, _pi]),
 }
 
 _lib = None
@@ -192,3 +205,15 @@ def symtridiag_eig_native(diag: np.ndarray, off: np.ndarray, vectors: bool):
                                              dptr(theta), dptr(G)))
     # G holds columns contiguously (column k at G[k*n]); transpose the view
     return theta[:n], (G.T if G is not None else None)
+
+
+def bidiag_sv2(alphas: np.ndarray, betas: np.ndarray) -> np.ndarray:
+    """Squared singular values (descending) of the (k+1) x k lower bidiagonal
+    with the given alphas (k) and betas (k+1; betas[0] unused), each to high
+    relative accuracy (eig.cpp ksvd_bidiag_sv2)."""
+    a = np.ascontiguousarray(alphas, dtype=np.float64)
+    b = np.ascontiguousarray(betas, dtype=np.float64)
+    k = int(a.shape[0])
+    theta = np.empty(max(k, 1))
+    check(load_library().ksvd_bidiag_sv2(k, dptr(a), dptr(b), dptr(theta)))
+    return theta[:k]

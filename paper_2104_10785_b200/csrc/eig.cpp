@@ -121,3 +121,75 @@ extern "C" int ksvd_symtridiag_eig(int n, const double* diag, const double* off,
   }
   return KSVD_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Singular values of the (k+1) x k lower bidiagonal B (alphas on the
+// diagonal, betas[1..k] below) to high RELATIVE accuracy: bisection on the
+// Golub-Kahan tridiagonal TGK = tridiag(0; a1, b2, a2, b3, ..., ak, b_{k+1})
+// (size 2k+1, eigenvalues +-sigma_i and 0; Demmel & Kahan 1990).  Used by
+// estimate_rank: theta_i = sigma_i^2 are the eigenvalues of B^T B
+// (rank.py:64), but the tiny ones come out accurate to a few ulps of
+// themselves instead of eps * ||T|| -- the relative rank threshold of
+// configuration 5, 1e-16 theta_1, sits exactly at that QL noise floor.
+namespace {
+
+struct TGK {
+  int k;
+  std::vector<double> e2;  // squared off-diagonals, 2k entries
+  double pivmin;
+
+  // number of singular values < x (x > 0)
+  int below(double x) const {
+    double q = -x;
+    int neg = q < 0;
+    for (double v : e2) {
+      q = -x - v / q;
+      if (std::fabs(q) < pivmin) q = -pivmin;
+      neg += q < 0;
+    }
+    return neg - (k + 1);
+  }
+};
+
+}  // namespace
+
+extern "C" int ksvd_bidiag_sv2(int k, const double* alphas, const double* betas, double* theta) {
+  if (k <= 0) return ksvd_set_error_from_host(KSVD_ECONFIG, "empty bidiagonal");
+  TGK t;
+  t.k = k;
+  t.e2.resize(2 * (size_t)k);
+  double emax = 0.0, gersh = 0.0;
+  for (int i = 0; i < k; ++i) {
+    const double a = std::fabs(alphas[i]), b = std::fabs(betas[i + 1]);
+    t.e2[2 * i] = a * a;
+    t.e2[2 * i + 1] = b * b;
+    emax = std::max(emax, std::max(a, b));
+  }
+  for (int i = 0; i < 2 * k; ++i) {  // Gershgorin bound of TGK
+    const double l = i > 0 ? std::sqrt(t.e2[i - 1]) : 0.0;
+    gersh = std::max(gersh, l + std::sqrt(t.e2[i]));
+  }
+  if (!std::isfinite(gersh)) return ksvd_set_error_from_host(KSVD_ENUMERIC, "non-finite bidiagonal");
+  t.pivmin = DBL_MIN * std::max(1.0, emax * emax);
+  std::vector<double> sv(k);
+  for (int j = 0; j < k; ++j) {  // j-th smallest singular value
+    double lo = 0.0, hi = gersh * (1.0 + 4 * DBL_EPSILON) + DBL_MIN;
+    for (int it = 0; it < 400; ++it) {
+      if (hi - lo <= 4 * DBL_EPSILON * hi || hi < 1e-300) break;
+      double mid;
+      if (lo == 0.0)
+        mid = hi * (hi > 1e-280 ? 1e-3 : 0.5);  // coarse descent to the scale
+      else if (hi > 2.0 * lo)
+        mid = std::sqrt(lo * hi);  // geometric bisection
+      else
+        mid = 0.5 * (lo + hi);
+      if (t.below(mid) <= j)
+        lo = mid;
+      else
+        hi = mid;
+    }
+    sv[j] = 0.5 * (lo + hi);
+  }
+  for (int j = 0; j < k; ++j) theta[j] = sv[k - 1 - j] * sv[k - 1 - j];  // descending
+  return KSVD_OK;
+}

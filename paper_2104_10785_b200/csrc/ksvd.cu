@@ -24,6 +24,7 @@
 #include <string>
 #include <vector>
 
+#include "gen.cuh"
 #include "kernels.cuh"
 #include "ksvd.h"
 
@@ -141,7 +142,7 @@ static int launch(ksvd_ctx* c, int cls, Kern kernel, dim3 grid, dim3 block,
 }
 
 static int allreduce(ksvd_ctx* c, double* buf, size_t count) {
-  if (c->nranks <= 1 || count == 0) return 0;
+  if (!c->comm || count == 0) return 0;
   NK(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, c->comm, c->stream));
   return 0;
 }
@@ -175,6 +176,9 @@ struct ksvd_mat {
   // plain-product scratch
   double *dx = nullptr, *dy = nullptr;
   DevState* st0 = nullptr;  // always-running state for plain products
+  // generator factors (ksvd_matrix_generate): Ps = P diag(s) local rows, Q
+  double *gen_ps = nullptr, *gen_q = nullptr;
+  int gen_r = 0;
 };
 
 static size_t esize(int dtype) { return dtype == KSVD_F32 ? 4 : 8; }
@@ -245,6 +249,8 @@ static int free_matrix(ksvd_mat* M) {
   cudaFree(M->dx);
   cudaFree(M->dy);
   cudaFree(M->st0);
+  cudaFree(M->gen_ps);
+  cudaFree(M->gen_q);
   delete M;
   return 0;
 }
@@ -311,7 +317,7 @@ static int enqueue_gemv_t(ksvd_mat* M, const double* q_src, const double* q_scal
     CK(cudaMemsetAsync(M->part_t, 0, sizeof(double) * M->n_pad, c->stream));
   }
   const int nsplit = M->mloc > 0 ? (int)pt.nsplit : 1;
-  const bool multi = c->nranks > 1;
+  const bool multi = c->comm != nullptr;
   if (!finalize && !multi) return 0;  // fused into the caller's k_cgs2_coop
   TRY(launch(c, KC_FIN, k_gemv_t_finalize, dim3((unsigned)cdiv(M->n_pad, 32)),
              dim3(kThreads), 0, (const double*)M->part_t, M->n_pad, nsplit, M->n,
@@ -377,7 +383,7 @@ static int cgs_impl(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int n
                     int side) {
   const int64_t nrb = std::max<int64_t>(1, cdiv(L, 32 * RPL));
   TRY(ensure_cgs(c->stream, W, nrb, ncols));
-  const bool multi = sharded && c->nranks > 1;
+  const bool multi = sharded && c->comm != nullptr;
   double* part = W->part;
   const dim3 grid((unsigned)nrb), block(kThreads);
   auto rows = k_cgs_rows<RPL>;
@@ -428,7 +434,7 @@ static bool coop_enabled(const ksvd_ctx* c, int ncols) {
     const char* e = getenv("KSVD_COOP");
     return e && strcmp(e, "0") == 0;
   }();
-  return !off && c->nranks == 1 && ncols <= kCoopMaxCols;
+  return !off && c->comm == nullptr && ncols <= kCoopMaxCols;
 }
 
 static int coop_max_ctas(ksvd_ctx* c) {
@@ -788,6 +794,136 @@ static int multi_rhs(ksvd_mat* M, const double* X, int64_t ldx, int k, const dou
   return enqueue_multi_rhs<double>(M, X, ldx, k, sigma, Y, ldy);
 }
 
+
+// ---------------------------------------------------------------------------
+// synthetic matrices (BASELINE.json configs 3-5)
+
+// Cholesky G = L L^T (lower) and R^{-1} = (L^T)^{-1} (upper, row-major).
+static int chol_rinv(int r, const std::vector<double>& G, std::vector<double>& Rinv) {
+  std::vector<double> L((size_t)r * r, 0.0);
+  for (int j = 0; j < r; ++j) {
+    double d = G[(size_t)j * r + j];
+    for (int k = 0; k < j; ++k) d -= L[(size_t)j * r + k] * L[(size_t)j * r + k];
+    if (!(d > 0)) return set_err(KSVD_ENUMERIC, "generator: Gram matrix not positive definite");
+    const double ljj = std::sqrt(d);
+    L[(size_t)j * r + j] = ljj;
+    for (int i = j + 1; i < r; ++i) {
+      double v = G[(size_t)i * r + j];
+      for (int k = 0; k < j; ++k) v -= L[(size_t)i * r + k] * L[(size_t)j * r + k];
+      L[(size_t)i * r + j] = v / ljj;
+    }
+  }
+  // Linv (lower) by forward substitution, then Rinv = Linv^T
+  std::vector<double> Linv((size_t)r * r, 0.0);
+  for (int c = 0; c < r; ++c) {
+    for (int i = c; i < r; ++i) {
+      double v = (i == c) ? 1.0 : 0.0;
+      for (int k = c; k < i; ++k) v -= L[(size_t)i * r + k] * Linv[(size_t)k * r + c];
+      Linv[(size_t)i * r + c] = v / L[(size_t)i * r + i];
+    }
+  }
+  Rinv.assign((size_t)r * r, 0.0);
+  for (int i = 0; i < r; ++i)
+    for (int j = 0; j < r; ++j) Rinv[(size_t)i * r + j] = Linv[(size_t)j * r + i];
+  return 0;
+}
+
+// X (rows x r, row-major) <- orthonormal columns by CholeskyQR2; the Gram
+// matrix is all-reduced across ranks when `sharded`.
+static int cholqr2(ksvd_ctx* c, double* X, int64_t rows, int r, bool sharded) {
+  cudaStream_t s = c->stream;
+  const int64_t splits = std::max<int64_t>(1, std::min<int64_t>(256, cdiv(rows, 4096)));
+  const int64_t rps = cdiv(std::max<int64_t>(rows, 1), splits);
+  double *part = nullptr, *G = nullptr, *Rd = nullptr, *Y = nullptr;
+  CK(cudaMallocAsync(&part, sizeof(double) * splits * r * r, s));
+  CK(cudaMallocAsync(&G, sizeof(double) * r * r, s));
+  CK(cudaMallocAsync(&Rd, sizeof(double) * r * r, s));
+  CK(cudaMallocAsync(&Y, sizeof(double) * std::max<int64_t>(rows, 1) * r, s));
+  std::vector<double> Gh((size_t)r * r), Rinv;
+  for (int pass = 0; pass < 2; ++pass) {
+    if (rows > 0) {
+      const dim3 g((unsigned)cdiv(r, kGramT), (unsigned)cdiv(r, kGramT), (unsigned)splits);
+      TRY(launch(c, KC_OTHER, k_gram_part, g, dim3(kThreads), 0, (const double*)X, rows, r,
+                 rps, part));
+      TRY(launch(c, KC_OTHER, k_gram_reduce, dim3((unsigned)cdiv((int64_t)r * r, kThreads)),
+                 dim3(kThreads), 0, (const double*)part, (int)splits, r, G));
+    } else {
+      CK(cudaMemsetAsync(G, 0, sizeof(double) * r * r, s));
+    }
+    if (sharded) TRY(allreduce(c, G, (size_t)r * r));
+    CK(cudaMemcpyAsync(Gh.data(), G, sizeof(double) * r * r, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    TRY(chol_rinv(r, Gh, Rinv));
+    CK(cudaMemcpyAsync(Rd, Rinv.data(), sizeof(double) * r * r, cudaMemcpyHostToDevice, s));
+    if (rows > 0) {
+      const dim3 g((unsigned)cdiv(r, kGT), (unsigned)cdiv(rows, kGT));
+      TRY(launch(c, KC_OTHER, k_gen_gemm<false, 0>, g, dim3(kThreads), 0, rows, (int64_t)r, r,
+                 (const double*)X, (int64_t)r, (const double*)Rd, (int64_t)r, (void*)Y,
+                 (int64_t)r, 0.0, (uint64_t)0, (int64_t)0, (int64_t)0));
+      CK(cudaMemcpyAsync(X, Y, sizeof(double) * rows * r, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  for (void* p : {(void*)part, (void*)G, (void*)Rd, (void*)Y}) CK(cudaFreeAsync(p, s));
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+static int generate_into(ksvd_mat* M, const ksvd_gen_spec* sp) {
+  ksvd_ctx* c = M->ctx;
+  cudaStream_t s = c->stream;
+  const int r = sp->rank;
+  std::vector<double> sv(r);
+  for (int i = 1; i <= r; ++i) {
+    switch (sp->spectrum) {
+      case KSVD_SPEC_HARMONIC: sv[i - 1] = sp->s0 / i; break;
+      case KSVD_SPEC_EXP: sv[i - 1] = sp->s0 * std::exp(-(double)i / sp->p); break;
+      default:
+        sv[i - 1] = r > 1 ? sp->s0 * std::pow(10.0, -sp->p * (double)(i - 1) / (double)(r - 1))
+                          : sp->s0;
+    }
+  }
+  const int64_t ml = M->mloc, n = M->n;
+  CK(cudaMalloc(&M->gen_ps, sizeof(double) * std::max<int64_t>(ml, 1) * r));
+  CK(cudaMalloc(&M->gen_q, sizeof(double) * n * r));
+  M->gen_r = r;
+  const unsigned gg = (unsigned)std::min<int64_t>(c->sms * 8, 65535);
+  if (ml > 0)
+    TRY(launch(c, KC_OTHER, k_gen_gauss, dim3(gg), dim3(kThreads), 0, M->gen_ps, ml, r,
+               (uint64_t)sp->seed, (uint32_t)KSVD_GEN_TAG_LEFT, M->row0));
+  TRY(launch(c, KC_OTHER, k_gen_gauss, dim3(gg), dim3(kThreads), 0, M->gen_q, n, r,
+             (uint64_t)sp->seed, (uint32_t)KSVD_GEN_TAG_RIGHT, (int64_t)0));
+  TRY(cholqr2(c, M->gen_ps, ml, r, true));
+  TRY(cholqr2(c, M->gen_q, n, r, false));
+  double* sd = nullptr;
+  CK(cudaMallocAsync(&sd, sizeof(double) * r, s));
+  CK(cudaMemcpyAsync(sd, sv.data(), sizeof(double) * r, cudaMemcpyHostToDevice, s));
+  if (ml > 0)
+    TRY(launch(c, KC_OTHER, k_scale_cols, dim3(gg), dim3(kThreads), 0, M->gen_ps, ml, r,
+               (const double*)sd));
+  CK(cudaFreeAsync(sd, s));
+  const size_t es = esize(M->dtype);
+  if (ml > 0) {
+    CK(cudaMemsetAsync(M->A, 0, (size_t)ml * M->lda * es, s));
+    // rows in slabs of 65535 CTA rows (grid.y limit)
+    const int64_t slab = (int64_t)65535 * kGT;
+    for (int64_t i0 = 0; i0 < ml; i0 += slab) {
+      const int64_t rows = std::min(slab, ml - i0);
+      const dim3 g((unsigned)cdiv(n, kGT), (unsigned)cdiv(rows, kGT));
+      void* dst = (char*)M->A + (size_t)i0 * M->lda * es;
+      if (M->dtype == KSVD_F32)
+        TRY(launch(c, KC_OTHER, k_gen_gemm<true, 2>, g, dim3(kThreads), 0, rows, n, r,
+                   (const double*)(M->gen_ps + i0 * r), (int64_t)r, (const double*)M->gen_q,
+                   (int64_t)r, dst, M->lda, sp->noise, (uint64_t)sp->seed, M->row0 + i0, n));
+      else
+        TRY(launch(c, KC_OTHER, k_gen_gemm<true, 1>, g, dim3(kThreads), 0, rows, n, r,
+                   (const double*)(M->gen_ps + i0 * r), (int64_t)r, (const double*)M->gen_q,
+                   (int64_t)r, dst, M->lda, sp->noise, (uint64_t)sp->seed, M->row0 + i0, n));
+    }
+  }
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
 // ---------------------------------------------------------------------------
 // C ABI
 extern "C" {
@@ -841,6 +977,12 @@ int ksvd_ctx_create(int device, int rank, int nranks, const char* uid, ksvd_ctx*
     ncclUniqueId id;
     memcpy(&id, uid, sizeof id);
     NK(ncclCommInitRank(&c->comm, nranks, id, rank));
+  } else if (getenv("KSVD_FORCE_NCCL")) {
+    // test hook: a 1-rank communicator exercises the multi-rank code path
+    // (all-reduces between the kernels) on a single GPU
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    NK(ncclCommInitRank(&c->comm, 1, id, 0));
   }
   *out = c;
   return 0;
@@ -974,6 +1116,53 @@ int ksvd_matrix_from_device(ksvd_ctx* c, const void* rows, int64_t m, int64_t n,
                             int64_t row0, int64_t mloc, int64_t src_ld, int dtype,
                             ksvd_mat** out) {
   return matrix_new(c, rows, m, n, row0, mloc, src_ld, dtype, cudaMemcpyDeviceToDevice, out);
+}
+
+int ksvd_matrix_generate(ksvd_ctx* c, const ksvd_gen_spec* sp, ksvd_mat** out) {
+  if (!sp || sp->m < 1 || sp->n < 1 || sp->rank < 1 || sp->rank > std::min(sp->m, sp->n))
+    return set_err(KSVD_ECONFIG, "generator: need m, n >= 1 and 1 <= rank <= min(m, n)");
+  if (sp->dtype != KSVD_F64 && sp->dtype != KSVD_F32)
+    return set_err(KSVD_ECONFIG, "generator: dtype %d", sp->dtype);
+  if (sp->spectrum < 0 || sp->spectrum > 2)
+    return set_err(KSVD_ECONFIG, "generator: spectrum %d", sp->spectrum);
+  CK(cudaSetDevice(c->device));
+  const int64_t base = sp->m / c->nranks, extra = sp->m % c->nranks;
+  const int64_t row0 = c->rank * base + std::min<int64_t>(c->rank, extra);
+  const int64_t mloc = base + (c->rank < extra ? 1 : 0);
+  auto* M = new ksvd_mat();
+  M->ctx = c;
+  M->m = sp->m;
+  M->n = sp->n;
+  M->row0 = row0;
+  M->mloc = mloc;
+  M->dtype = sp->dtype;
+  const int64_t es = (int64_t)esize(sp->dtype);
+  M->lda = rup(sp->n, 512 / es);
+  M->n_pad = rup(sp->n, 64);
+  M->m_pad = rup(std::max<int64_t>(mloc, 1), 64);
+  int rc = alloc_matrix_buffers(M);
+  if (!rc) rc = generate_into(M, sp);
+  if (rc) {
+    free_matrix(M);
+    return rc;
+  }
+  *out = M;
+  return 0;
+}
+
+int ksvd_matrix_gen_factors(ksvd_mat* M, double* Ps_local, double* Q, int* r) {
+  ksvd_ctx* c = M->ctx;
+  CK(cudaSetDevice(c->device));
+  if (r) *r = M->gen_r;
+  if (!M->gen_r) return set_err(KSVD_ECONFIG, "matrix was not generated on the device");
+  if (Ps_local && M->mloc > 0)
+    CK(cudaMemcpyAsync(Ps_local, M->gen_ps, sizeof(double) * M->mloc * M->gen_r,
+                       cudaMemcpyDeviceToHost, c->stream));
+  if (Q)
+    CK(cudaMemcpyAsync(Q, M->gen_q, sizeof(double) * M->n * M->gen_r, cudaMemcpyDeviceToHost,
+                       c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
 }
 
 int ksvd_matrix_free(ksvd_mat* M) { return free_matrix(M); }

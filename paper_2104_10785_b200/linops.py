@@ -194,6 +194,18 @@ class DeviceMatrix(LinearOperator):
             self.handle, out.ctypes.data if self.m_local else None))
         return out
 
+    def gen_factors(self):
+        """(Ps_local, Q) of a device-generated matrix: Ps = P diag(s) for this
+        rank's rows (m_local x r) and Q (n x r), for oracle regeneration."""
+        lib = _lib.load_library()
+        r = C.c_int()
+        _lib.check(lib.ksvd_matrix_gen_factors(self.handle, None, None, C.byref(r)))
+        ps = np.empty((self.m_local, r.value))
+        q = np.empty((self.shape[1], r.value))
+        _lib.check(lib.ksvd_matrix_gen_factors(self.handle, _lib.dptr(ps), _lib.dptr(q),
+                                               C.byref(r)))
+        return ps, q
+
     def free(self):
         self._fin()
 

@@ -12,8 +12,13 @@ from __future__ import annotations
 
 import numpy as np
 
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+from . import _lib
 from .errors import ConfigError
-from .linops import substream
+from .linops import DeviceMatrix, row_partition, substream
 
 GAUSS, SYNTH_LEFT, SYNTH_RIGHT, BENCH_MATRIX = 1, 2, 3, 12  # reference tags
 
@@ -61,8 +66,60 @@ def config2_matrix(seed: int = 1, m: int = 20000, n: int = 5000, r: int = 137,
     return A.astype(dtype, copy=False)
 
 
-# (call, kwargs) of each BASELINE.json config that the host can build
+@dataclass(frozen=True)
+class GenSpec:
+    """A = P diag(s) Q^T + noise G generated on the device (include/ksvd.h
+    ksvd_gen_spec); spectrum "harmonic" s_i = s0/i, "exp" s_i = s0 e^(-i/p),
+    "geom" s_i = s0 10^(-p (i-1)/(r-1))."""
+
+    m: int
+    n: int
+    rank: int
+    seed: int
+    spectrum: str
+    s0: float
+    p: float = 0.0
+    noise: float = 0.0
+    dtype: str = "f64"
+
+    def scaled(self, m: int, n: int) -> "GenSpec":
+        """Same recipe at another size (noise rescaled with 1/sqrt(n) where
+        the config defines it that way)."""
+        noise = self.noise * math.sqrt(self.n) / math.sqrt(n) if self.spectrum != "geom" \
+            else self.noise
+        return GenSpec(m, n, min(self.rank, m, n), self.seed, self.spectrum, self.s0, self.p,
+                       noise, self.dtype)
+
+
+# BASELINE.json configs 3-5 (SURVEY.md 8(d)); configs 1-2 are host-built
+BASELINE_SPECS = {
+    3: GenSpec(200_000, 20_000, 50, 2, "harmonic", 1000.0, 0.0, 1e-3 / math.sqrt(20_000)),
+    4: GenSpec(1_000_000, 40_000, 100, 3, "exp", 100.0, 20.0, 1e-4 / math.sqrt(40_000), "f32"),
+    5: GenSpec(500_000, 20_000, 300, 4, "geom", 1.0, 3.0, 1e-12),
+}
+
+# (call, kwargs) of each BASELINE.json config
 BASELINE_CALLS = {
     1: dict(kind="fsvd", k=30, r=10, eps=1e-10, seed=0),
     2: dict(kind="rank", eps=1e-6, mode="relative", seed=1),
+    3: dict(kind="fsvd", k=60, r=20, eps=1e-8, seed=2),
+    4: dict(kind="fsvd", k=96, r=32, eps=1e-8, seed=3),
+    5: dict(kind="rank", eps=1e-8, mode="relative", seed=4),
 }
+
+
+def generate(spec: GenSpec, ctx: _lib.Context | None = None) -> DeviceMatrix:
+    """Generate A on the device (this rank's row shard)."""
+    ctx = ctx or _lib.get_context()
+    code = {"harmonic": _lib.SPEC_HARMONIC, "exp": _lib.SPEC_EXP, "geom": _lib.SPEC_GEOM}
+    if spec.spectrum not in code:
+        raise ConfigError(f"unknown spectrum {spec.spectrum!r}")
+    cs = _lib.GenSpec(m=spec.m, n=spec.n, rank=spec.rank,
+                      dtype=_lib.KSVD_F32 if spec.dtype == "f32" else _lib.KSVD_F64,
+                      seed=spec.seed, spectrum=code[spec.spectrum], pad=0, s0=spec.s0,
+                      p=spec.p, noise=spec.noise)
+    h = C.c_void_p()
+    _lib.check(_lib.load_library().ksvd_matrix_generate(ctx.handle, C.byref(cs), C.byref(h)))
+    r0, ml = row_partition(spec.m, ctx.nranks, ctx.rank)
+    return DeviceMatrix(h, ctx, (spec.m, spec.n), r0, ml,
+                        np.float32 if spec.dtype == "f32" else np.float64)

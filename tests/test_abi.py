@@ -78,3 +78,26 @@ def test_no_cpu_fallback_without_gpu():
     _lib.set_context(None)
     with pytest.raises(RuntimeError):
         fsvd(np.eye(4), k=2, r=1)
+
+
+def test_bidiag_sv2_relative_accuracy():
+    """Rank estimation's tiny bidiagonal SVD (eig.cpp ksvd_bidiag_sv2) is
+    accurate to a few ulps of each value, also for a graded spectrum whose
+    small values a QL on B^T B only resolves to eps*||T|| (checked against
+    40-digit arithmetic)."""
+    mpmath = pytest.importorskip("mpmath")
+    mpmath.mp.dps = 50
+    rng = np.random.default_rng(11)
+    for k, graded in [(1, False), (7, False), (40, False), (25, True)]:
+        a = rng.random(k) + 0.1
+        b = rng.random(k + 1) + 0.1
+        if graded:
+            a = a * 10.0 ** (-0.9 * np.arange(k))
+            b[1:] = b[1:] * 10.0 ** (-0.9 * np.arange(k))
+        B = np.zeros((k + 1, k))
+        B[np.arange(k), np.arange(k)] = a
+        B[np.arange(1, k + 1), np.arange(k)] = b[1:]
+        ref = sorted((float(x) ** 2 for x in mpmath.svd_r(mpmath.matrix(B.tolist()),
+                                                            compute_uv=False)), reverse=True)
+        got = _lib.bidiag_sv2(a, b)
+        assert np.max(np.abs(got - ref) / np.array(ref)) < 1e-14, (k, graded)

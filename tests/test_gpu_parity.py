@@ -277,10 +277,12 @@ print(json.dumps(out))
 """
 
 
-@pytest.mark.parametrize("env", [{"KSVD_TILE": "0"}, {"KSVD_COOP": "0"}, {}])
+@pytest.mark.parametrize("env", [{"KSVD_TILE": "0"}, {"KSVD_COOP": "0"}, {"KSVD_FORCE_NCCL": "1"}, {}])
 def test_cgs_paths_agree(env):
     """The tile-resident, global-load cooperative and multi-kernel CGS2
-    paths (selected at load time) all meet the parity bar."""
+    paths (selected at load time) all meet the parity bar; KSVD_FORCE_NCCL
+    runs the multi-rank code path (NCCL all-reduces between the kernels)
+    over a 1-rank communicator."""
     import json
     import os
     import subprocess
