@@ -3,26 +3,30 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
-One bench "step" is one call of the reference entry point on the
-configuration (default: config 2, `estimate_rank` of a 20000 x 5000 f64
-matrix with eps = 1e-6 relative, BASELINE.json configs[1]).  Metric: GK
-steps/s (k' GK iterations per call / time per call); the JSON line also
-carries time-to-result, effective HBM GB/s (2 m n bytes k' / time), the
-roofline of the A-streaming kernels, the CPU baseline and the end-to-end
-number through the public API with host buffers.
+One bench "step" is one call of the reference entry point on configuration
+C of BASELINE.json (default C = 2, `estimate_rank` of a 20000 x 5000 f64
+matrix with eps = 1e-6 relative -- configs[1]).  Configs 1-2 are built on
+the host (numpy); 3-5 are generated in HBM (include/ksvd_gen.h; they do not
+fit a host oracle).  Metric: GK steps/s = GK iterations (k') per call /
+time per call; the line also carries the time to result, the effective HBM
+bandwidth 2 m n bytes k' / time, the roofline of the A-streaming kernels,
+the CPU baseline and the end-to-end number through the public API.
 
-  value : device-resident A (uploaded once), CUDA events on the library
-          stream around exactly K calls, barrier + sync on both sides,
-          max over ranks.  A (800 MB) is larger than L2 (126 MB), so every
-          pass streams HBM; no explicit flush needed.
-  e2e   : `estimate_rank(A_host)` with A in pinned host memory: upload of
-          this rank's rows + the run + the result read-back, per step.
-  roofline : per-launch CUDA-event durations of the gemv_n / gemv_t
-          kernels measured in a profiled repeat of the same K calls;
-          algorithmic bytes per launch = m_local * n * 8.
+  value    : device-resident A, CUDA events on the library stream around
+             exactly K calls, barrier + sync on both sides, max over ranks.
+             A is larger than L2 (126 MB) for every config but config 1
+             (16 MB, L2-resident: latency-bound by construction).
+  e2e      : host configs -- `entry(A_host)` with A in pinned host memory:
+             upload of this rank's rows + the run + the result read-back;
+             device configs -- the public call on the resident matrix plus
+             the read-back of U, sigma, V / the rank report (A has no host
+             copy at these sizes).
+  roofline : per-launch CUDA-event durations of gemv_n / gemv_t measured in
+             a profiled repeat of the same calls; algorithmic bytes per
+             launch = m_local * n * sizeof(A).
   --impl reference : the CPU oracle port of the reference algorithm
-          (oracle/krylov_oracle.py, numpy/OpenBLAS on all host cores) on the
-          same matrix; each step is a bounded sample: 48 GK iterations.
+             (oracle/krylov_oracle.py, numpy/OpenBLAS on all host cores);
+             each step is a bounded sample (see `sample` in the line).
 """
 
 from __future__ import annotations
@@ -45,7 +49,8 @@ METRIC = ("GK steps/s & time to top-k SVD; A·v+Aᵀu HBM GB/s vs roofline "
           "at 1/2/4/8 GPU")
 UNIT = "GK steps/s"
 FALLBACK_HBM_GBS = 6650.0
-REF_SAMPLE_STEPS = 48
+REF_SAMPLE_STEPS = 48   # GK iterations per reference-arm step (host configs)
+REF_SAMPLE_ROWS = 8192  # rows of the CPU sample for device-generated configs
 
 
 def parse():
@@ -53,7 +58,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -63,21 +68,33 @@ def parse():
 def workload(cfg_id):
     from paper_2104_10785_b200 import synth
 
+    call = dict(synth.BASELINE_CALLS[cfg_id])
     if cfg_id == 1:
-        return dict(name="config1: fsvd k=30 r=10 eps=1e-10 of 2000x1000 f64 "
-                    "(U diag(10^(-4(i-1)/999)) V^T, seed 0)",
-                    m=2000, n=1000, make=lambda: synth.config1_matrix(seed=0),
-                    kind="fsvd", k=30, r=10, eps=1e-10, seed=0)
-    return dict(name="config2: estimate_rank eps=1e-6 relative of 20000x5000 f64 "
-                "(X Y^T + E, rank 137, seed 1)",
-                m=20000, n=5000, make=None, kind="rank", eps=1e-6, mode="relative", seed=1)
+        W = dict(name="config1: fsvd k=30 r=10 eps=1e-10 of 2000x1000 f64 "
+                 "(U diag(10^(-4(i-1)/999)) V^T, seed 0)", m=2000, n=1000, esize=8,
+                 source="host")
+    elif cfg_id == 2:
+        W = dict(name="config2: estimate_rank eps=1e-6 relative of 20000x5000 f64 "
+                 "(X Y^T + E, rank 137, seed 1)", m=20000, n=5000, esize=8, source="host")
+    else:
+        spec = synth.BASELINE_SPECS[cfg_id]
+        what = "fsvd k=%d r=%d" % (call["k"], call["r"]) if call["kind"] == "fsvd" else \
+            "estimate_rank eps=%g %s" % (call["eps"], call["mode"])
+        W = dict(name=f"config{cfg_id}: {what} of {spec.m}x{spec.n} {spec.dtype} "
+                 f"(P diag(s) Q^T + noise, rank {spec.rank}, {spec.spectrum} spectrum, "
+                 f"seed {spec.seed}; generated in HBM)",
+                 m=spec.m, n=spec.n, esize=4 if spec.dtype == "f32" else 8, source="device",
+                 spec=spec)
+    W.update(call)
+    W["id"] = cfg_id
+    return W
 
 
-def make_matrix(W, out=None):
+def host_matrix(W, out=None):
     from paper_2104_10785_b200 import synth
 
-    if W["kind"] == "fsvd":
-        A = W["make"]()
+    if W["id"] == 1:
+        A = synth.config1_matrix(seed=0)
         if out is not None:
             out[...] = A
             return out
@@ -86,11 +103,14 @@ def make_matrix(W, out=None):
 
 
 def call(K, W, A):
-    """One bench step through the public API; returns GK iterations done."""
+    """One bench step through the public API; returns (GK iterations, D2H bytes)."""
     if W["kind"] == "fsvd":
         psvd = K.fsvd(A, k=W["k"], r=W["r"],
                       cfg=K.BidiagConfig(k_max=W["k"], eps=W["eps"], seed=W["seed"]))
-        return W["k"], psvd.sigma.nbytes + psvd.U.nbytes + psvd.V.nbytes
+        fsvd_mod = sys.modules["paper_2104_10785_b200.fsvd"]
+
+        # k' = the GK iterations the run performed (k unless it broke down)
+        return fsvd_mod.last_k_prime, psvd.sigma.nbytes + psvd.U.nbytes + psvd.V.nbytes
     rep = K.estimate_rank(A, eps=W["eps"], mode=W["mode"], cfg=K.BidiagConfig(k_max=1, seed=W["seed"]))
     return rep.k_prime, 8 * (2 * rep.k_prime + 1)
 
@@ -155,15 +175,6 @@ def host_cores():
         return os.cpu_count() or 1
 
 
-def cpu_rank_sample(A, W, k_max):
-    """Oracle GK loop truncated at k_max steps: (gk steps, seconds)."""
-    from oracle import krylov_oracle as O
-
-    t0 = time.perf_counter()
-    g = O.gk_oracle(A, k_max, eps=1e-8, seed=W["seed"])
-    return g.k_prime, time.perf_counter() - t0
-
-
 def blas_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -172,6 +183,39 @@ def blas_threads():
         return max((i.get("num_threads", 1) for i in info), default=host_cores())
     except Exception:  # noqa: BLE001
         return host_cores()
+
+
+def cpu_sample(W, A_host=None):
+    """Time the oracle (numpy port of the reference) on a bounded sample.
+    Returns (GK steps/s for the full configuration, description, seconds)."""
+    from oracle import krylov_oracle as O
+
+    bytes_step_full = 2.0 * W["m"] * W["n"] * 8  # the reference computes in f64
+    if W["source"] == "host":
+        A = A_host if A_host is not None else host_matrix(W)
+        if W["kind"] == "fsvd":
+            t0 = time.perf_counter()
+            O.fsvd_oracle(A, W["k"], W["r"], eps=W["eps"], seed=W["seed"])
+            dt = time.perf_counter() - t0
+            return W["k"] / dt, "one full oracle fsvd call on the config matrix", dt
+        t0 = time.perf_counter()
+        g = O.gk_oracle(A, min(REF_SAMPLE_STEPS, min(A.shape)), eps=1e-8, seed=W["seed"])
+        dt = time.perf_counter() - t0
+        return (g.k_prime / dt,
+                f"oracle GK loop truncated at {REF_SAMPLE_STEPS} iterations on the config matrix",
+                dt)
+    # device-generated configs: a host sample of the same width, rate
+    # extrapolated by bytes (the CPU products are bandwidth-bound)
+    rows = min(REF_SAMPLE_ROWS, W["m"])
+    Asamp = np.random.default_rng(W["seed"]).standard_normal((rows, W["n"]))
+    steps = 16
+    t0 = time.perf_counter()
+    O.gk_oracle(Asamp, steps, eps=1e-8, seed=W["seed"])
+    dt = time.perf_counter() - t0
+    gbps = 2.0 * rows * W["n"] * 8 * steps / dt / 1e9
+    return (gbps * 1e9 / bytes_step_full,
+            f"oracle GK loop, {steps} iterations on a {rows} x {W['n']} f64 sample of the same "
+            f"width ({gbps:.1f} GB/s), extrapolated to the full matrix by bytes per GK step", dt)
 
 
 def peak_hbm():
@@ -196,33 +240,23 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     W = workload(args.config)
-    A = make_matrix(W)
-    steps = []
+    A = host_matrix(W) if W["source"] == "host" else None
+    vals, secs, desc = [], [], ""
     for i in range(args.warmup + args.steps):
-        if W["kind"] == "fsvd":
-            from oracle import krylov_oracle as O
-
-            t0 = time.perf_counter()
-            O.fsvd_oracle(A, W["k"], W["r"], eps=W["eps"], seed=W["seed"])
-            kp, dt = W["k"], time.perf_counter() - t0
-        else:
-            kp, dt = cpu_rank_sample(A, W, REF_SAMPLE_STEPS)
+        v, desc, dt = cpu_sample(W, A)
         if i >= args.warmup:
-            steps.append((kp, dt))
-    tot_k = sum(k for k, _ in steps)
-    tot_t = sum(t for _, t in steps)
-    val = tot_k / tot_t
+            vals.append(v)
+            secs.append(dt)
+    val = statistics.fmean(vals)
     cores = blas_threads()
-    sample = (f"{REF_SAMPLE_STEPS} GK iterations (k_max={REF_SAMPLE_STEPS}) of the config "
-              "matrix per step" if W["kind"] == "rank" else "one full fsvd call per step")
     line = {
         "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / len(steps),
+        "warmup": args.warmup, "ms_per_step": 1e3 * statistics.fmean(secs),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
         "config": {"workload": W["name"], "m": W["m"], "n": W["n"], "parallelism": "host cpu"},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": sample},
+                         "sample": desc},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "effective_GBps": 2.0 * W["m"] * W["n"] * 8 * val / 1e9,
     }
@@ -231,12 +265,12 @@ def run_reference(args, rank, world):
 
 def run_ours(args, rank, world, dist):
     import paper_2104_10785_b200 as K
-    from paper_2104_10785_b200 import _lib
+    from paper_2104_10785_b200 import _lib, synth
     from paper_2104_10785_b200.dist import init_distributed
 
     ctx = init_distributed() if world > 1 else _lib.get_context()
     W = workload(args.config)
-    m, n = W["m"], W["n"]
+    m, n, es = W["m"], W["n"], W["esize"]
 
     def barrier():
         ctx.sync()
@@ -252,8 +286,12 @@ def run_ours(args, rank, world, dist):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    A = make_matrix(W)
-    op = K.DeviceMatrix.from_host(A)
+    A_host = None
+    if W["source"] == "host":
+        A_host = host_matrix(W)
+        op = K.DeviceMatrix.from_host(A_host)
+    else:
+        op = synth.generate(W["spec"])
     m_local = op.m_local
 
     # ---- value: device-resident A ----
@@ -273,18 +311,18 @@ def run_ours(args, rank, world, dist):
     launches = ctx.launch_count()
     gk_steps = sum(kps)
     value = gk_steps / (ms / 1e3)
-    eff_gbps = 2.0 * m * n * 8 * gk_steps / (ms / 1e3) / 1e9
+    eff_gbps = 2.0 * m * n * es * gk_steps / (ms / 1e3) / 1e9
 
-    # ---- roofline: profiled repeat of the same K calls ----
+    # ---- roofline: profiled repeat of the same calls ----
     barrier()
     ctx.reset_stats()
     ctx.set_profiling(True)
-    for _ in range(args.steps):
+    for _ in range(max(1, min(args.steps, 3 if W["source"] == "device" else args.steps))):
         call(K, W, op)
     ctx.set_profiling(False)
     stats = {c: ctx.kernel_stats(c) for c in range(5)}
     barrier()
-    bytes_launch = float(m_local) * n * 8
+    bytes_launch = float(m_local) * n * es
     nn, msn = stats[0]
     nt, mst = stats[1]
     peak, peak_src = peak_hbm()
@@ -304,25 +342,30 @@ def run_ours(args, rank, world, dist):
                                  zip(["gemv_n", "gemv_t", "cgs", "other", "finalize"],
                                      stats.values())} if tot_prof else None,
         "frac_of_nominal_8TBps": achieved / 8000.0,
+        "frac_of_measured_read_7264GBps": achieved / 7263.6,
     }
 
-    # ---- e2e: public API with host (pinned) buffers ----
+    # ---- e2e through the public API ----
     e2e = None
     if not args.no_e2e:
-        import torch
+        t_e2e, kps_e2e, d2h, h2d, kind = [], [], 0, 0, ""
+        if W["source"] == "host":
+            import torch
 
-        pinned = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
-        A_host = pinned.numpy()
-        A_host[...] = A
-        for _ in range(min(args.warmup, 1)):
-            call(K, W, A_host)
+            pinned = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
+            src = pinned.numpy()
+            src[...] = A_host
+            kind = "host pinned A uploaded every step"
+            h2d = int(m_local * n * 8 + m_local * 8)
+        else:
+            src = op
+            kind = "device-generated A (no host copy); start vector up, results down"
+            h2d = int(m_local * 8)
+        call(K, W, src)
         barrier()
-        t_e2e = []
-        kps_e2e = []
-        d2h = 0
         for _ in range(args.steps):
             ctx.mark(2)
-            kp, nb = call(K, W, A_host)
+            kp, nb = call(K, W, src)
             ctx.mark(3)
             ctx.sync()
             t_e2e.append(ctx.elapsed_ms(2, 3))
@@ -330,38 +373,26 @@ def run_ours(args, rank, world, dist):
             d2h = nb
         barrier()
         e_ms = max_over_ranks(sum(t_e2e))
-        e2e = {"value": sum(kps_e2e) / (e_ms / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(m_local * n * 8 + m_local * 8),
-               "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": e_ms / args.steps}
-        del pinned
+        e2e = {"value": sum(kps_e2e) / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms / args.steps, "kind": kind}
 
     # ---- CPU baseline (rank 0, N=1) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        if W["kind"] == "rank":
-            kp, dt = cpu_rank_sample(A, W, REF_SAMPLE_STEPS)
-            sample = f"oracle GK loop truncated at {REF_SAMPLE_STEPS} iterations on the config matrix"
-        else:
-            from oracle import krylov_oracle as O
-
-            t0 = time.perf_counter()
-            O.fsvd_oracle(A, W["k"], W["r"], eps=W["eps"], seed=W["seed"])
-            kp, dt = W["k"], time.perf_counter() - t0
-            sample = "one full oracle fsvd call"
-        cpu = {"value": kp / dt, "unit": UNIT, "cores": blas_threads(), "kind": "port",
-               "sample": sample, "seconds": dt}
+        v, desc, dt = cpu_sample(W, A_host)
+        cpu = {"value": v, "unit": UNIT, "cores": blas_threads(), "kind": "port",
+               "sample": desc, "seconds": dt}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
+            "dtype": "f64" if es == 8 else "f64 (f32 storage of A)", "data": "synthetic",
             "config": {"workload": W["name"], "m": m, "n": n,
                        "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
-                       "l2": "A (%.0f MB) > L2 (126 MB): every pass streams HBM"
-                             % (m * n * 8 / 1e6)},
+                       "l2": "A (%.0f MB) %s L2 (126 MB)" % (m * n * es / 1e6,
+                                                            ">" if m * n * es > 126e6 else "<=")},
             "time_to_result_s": ms / args.steps / 1e3,
             "gk_steps_per_call": kps[0] if kps else None,
             "effective_GBps": eff_gbps,

@@ -171,8 +171,24 @@ extern "C" int ksvd_bidiag_sv2(int k, const double* alphas, const double* betas,
   }
   if (!std::isfinite(gersh)) return ksvd_set_error_from_host(KSVD_ENUMERIC, "non-finite bidiagonal");
   t.pivmin = DBL_MIN * std::max(1.0, emax * emax);
-  std::vector<double> sv(k);
-  for (int j = 0; j < k; ++j) {  // j-th smallest singular value
+  // Large values: QL on B^T B (as the reference, fsvd.py:63-134) -- accurate
+  // to eps*||T|| absolutely, i.e. to ~1e-10 relative above 1e-6 theta_1.
+  // Tail below that: bisection on TGK, accurate to a few ulps of itself.
+  QL q;
+  q.n = k;
+  q.d.resize(k);
+  q.e.assign(k, 0.0);
+  for (int i = 0; i < k; ++i)
+    q.d[i] = alphas[i] * alphas[i] + betas[i + 1] * betas[i + 1];
+  for (int i = 0; i + 1 < k; ++i) q.e[i] = alphas[i + 1] * betas[i + 1];
+  if (!q.solve())
+    return ksvd_set_error_from_host(KSVD_ENUMERIC, "tridiagonal QL did not converge in 64 sweeps");
+  std::vector<double> th(q.d);
+  std::sort(th.begin(), th.end(), [](double a, double b) { return a > b; });
+  const double tau = 1e-6 * std::max(th[0], 0.0);
+  int tail = 0;
+  while (tail < k && th[k - 1 - tail] < tau) ++tail;
+  for (int j = 0; j < tail; ++j) {  // j-th smallest singular value
     double lo = 0.0, hi = gersh * (1.0 + 4 * DBL_EPSILON) + DBL_MIN;
     for (int it = 0; it < 400; ++it) {
       if (hi - lo <= 4 * DBL_EPSILON * hi || hi < 1e-300) break;
@@ -188,8 +204,10 @@ extern "C" int ksvd_bidiag_sv2(int k, const double* alphas, const double* betas,
       else
         hi = mid;
     }
-    sv[j] = 0.5 * (lo + hi);
+    const double sv = 0.5 * (lo + hi);
+    th[k - 1 - j] = sv * sv;
   }
-  for (int j = 0; j < k; ++j) theta[j] = sv[k - 1 - j] * sv[k - 1 - j];  // descending
+  std::sort(th.begin(), th.end(), [](double a, double b) { return a > b; });
+  for (int j = 0; j < k; ++j) theta[j] = th[j];
   return KSVD_OK;
 }

@@ -26,6 +26,8 @@ from .linops import PartialSvd, as_operator, shape_of
 DROP_REL = 1e-14
 # Residual cut of the left-vector filter (reference fsvd.py:137-142).
 DEPENDENT_TOL = 1e-2
+# k' of the most recent fsvd run in this process (bench instrumentation)
+last_k_prime = 0
 
 
 @dataclass(frozen=True)
@@ -86,7 +88,9 @@ def fsvd(A, k: int, r: int, cfg: BidiagConfig | None = None,
             f"need 1 <= r <= k <= min(m,n); got r={r}, k={k}, min(m,n)={min(m, n)}")
     cfg = BidiagConfig(k_max=k) if cfg is None else with_k_max(cfg, k)
     op = as_operator(A)
+    global last_k_prime
     run = run_gk(op, cfg)
+    last_k_prime = run.k_prime
     try:
         if run.degenerate:
             empty = PartialSvd(np.zeros((op.m_local, 0)), np.zeros(0), np.zeros((n, 0)),
