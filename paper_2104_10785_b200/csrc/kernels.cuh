@@ -92,6 +92,20 @@ __device__ __forceinline__ int warp_sum8_index(int lane) {
   return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
 // ---------------------------------------------------------------------------
 // 16-byte streaming loads of A.  A is read exactly once per pass, so it is
 // loaded through the non-coherent path without L1 allocation.
@@ -136,12 +150,13 @@ __device__ __forceinline__ void flag_nonfinite(DevState* st, double v, int step)
 // of the same rows, so a CTA reads long contiguous row segments.  Partials
 // per (chunk, row) go to part[chunk*m + row]; k_gemv_n_finalize adds them
 // in chunk order and applies - alpha q.
-template <typename TA, int U>
+template <typename TA, int U, int RB = 8>
 __global__ void __launch_bounds__(kThreads)
 k_gemv_n2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nchunks,
           int64_t rows_per_warp, const double* __restrict__ p_src,
           const double* __restrict__ p_scale, double* __restrict__ p_dst, int64_t n_true,
           double* __restrict__ part, const DevState* st) {
+  static_assert(RB % 8 == 0, "rows per iteration: multiple of 8");
   if (halted(st)) return;
   constexpr int V = AVec<TA>::V;
   constexpr int CW = 32 * U;
@@ -171,30 +186,188 @@ k_gemv_n2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nc
     }
   }
   const TA* base = A + ((int64_t)chunk * CW + lane) * V;
-  for (int64_t r = r_begin; r < r_end; r += 8) {
-    double v[8];
-    AVec<TA> a[8][U];
+  for (int64_t r = r_begin; r < r_end; r += RB) {
+    AVec<TA> a[RB][U];
 #pragma unroll
-    for (int rr = 0; rr < 8; ++rr) {
+    for (int rr = 0; rr < RB; ++rr) {
       const int64_t row = min(r + rr, r_end - 1);  // clamp: duplicate rows are discarded
 #pragma unroll
       for (int u = 0; u < U; ++u)
         if (live[u]) a[rr][u].load(base + row * lda + u * 32 * V);
     }
 #pragma unroll
-    for (int rr = 0; rr < 8; ++rr) {
-      double s = 0.0;
+    for (int h = 0; h < RB / 8; ++h) {
+      double v[8];
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (live[u]) {
+      for (int rr = 0; rr < 8; ++rr) {
+        double s = 0.0;
 #pragma unroll
-          for (int k = 0; k < V; ++k) s = fma(a[rr][u].get(k), pv[u][k], s);
-        }
-      v[rr] = s;
+        for (int u = 0; u < U; ++u)
+          if (live[u]) {
+#pragma unroll
+            for (int k = 0; k < V; ++k) s = fma(a[h * 8 + rr][u].get(k), pv[u][k], s);
+          }
+        v[rr] = s;
+      }
+      const double t = warp_sum8(v);
+      const int64_t row = r + h * 8 + warp_sum8_index(lane);
+      if ((lane & 3) == 0 && row < r_end) part[(int64_t)chunk * m + row] = t;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// gemv_n, TMA-fed (k_gemv_n3): w = A p   (bidiag.py:152)
+//
+// Persistent: one CTA per SM, 8 consumer warps + 1 producer warp.  Work
+// units are (column group of 8 chunks, 8 consecutive rows); CTA b takes the
+// contiguous unit range [b*N/G, (b+1)*N/G), so units walk down the rows of
+// one column group.  The producer streams each unit -- 8 row segments of
+// 8 KB, one bulk-async copy (cp.async.bulk) per row -- into a 3-stage
+// shared-memory ring guarded by full/empty mbarriers; consumer warp w owns
+// chunk w of the group: its slice of p sits in registers, it reads its
+// 1 KB of each row from shared memory, forms the 8 row partials and reduces
+// them with one warp_sum8.  A never passes through registers in flight, so
+// the kernel keeps 128 KB of loads outstanding per SM at low register cost.
+// Output layout = k_gemv_n2 (part[chunk*m + row]).
+constexpr int kN3Stages = 3;
+constexpr int kN3Rows = 8;
+constexpr int kN3Group = 8;       // chunks per column group = consumer warps
+constexpr int kN3U = 2;           // 16-byte vectors per lane per row
+constexpr int kN3CW = 32 * kN3U;  // vectors per chunk (1 KB)
+constexpr int kN3Threads = (kN3Group + 1) * 32;
+constexpr size_t kN3StageBytes = (size_t)kN3Rows * kN3Group * kN3CW * 16;  // 64 KB
+constexpr size_t kN3Smem = kN3Stages * kN3StageBytes;
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+template <typename TA>
+__global__ void __launch_bounds__(kN3Threads, 1)
+k_gemv_n3(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nchunks,
+          int64_t rows8, int64_t units, const double* __restrict__ p_src,
+          const double* __restrict__ p_scale, double* __restrict__ p_dst, int64_t n_true,
+          double* __restrict__ part, const DevState* st) {
+  if (halted(st)) return;
+  constexpr int V = AVec<TA>::V;
+  extern __shared__ __align__(1024) unsigned char n3_smem[];
+  __shared__ __align__(8) unsigned long long full[kN3Stages], empty[kN3Stages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t G = gridDim.x;
+  const int64_t u0 = units * blockIdx.x / G, u1 = units * (blockIdx.x + 1) / G;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kN3Stages; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), kN3Group);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kN3Group) {  // ---- producer
+    if (lane == 0) {
+      for (int64_t u = u0, it = 0; u < u1; ++u, ++it) {
+        const int s = (int)(it % kN3Stages);
+        const int64_t round = it / kN3Stages;
+        if (round > 0)
+          while (!mbar_try_wait(smem_u32(&empty[s]), (uint32_t)((round - 1) & 1))) {
+          }
+        const int64_t g = u / rows8, r0 = (u % rows8) * kN3Rows;
+        const int nr = (int)(m - r0 < kN3Rows ? m - r0 : kN3Rows);
+        const int64_t v0 = g * kN3Group * kN3CW;
+        const int64_t wv = nvec - v0 < kN3Group * kN3CW ? nvec - v0 : (int64_t)kN3Group * kN3CW;
+        const uint32_t bytes = (uint32_t)(wv * 16);
+        const uint32_t fb = smem_u32(&full[s]);
+        mbar_expect_tx(fb, bytes * (uint32_t)nr);
+        unsigned char* stage = n3_smem + (size_t)s * kN3StageBytes;
+        for (int rr = 0; rr < nr; ++rr)
+          bulk_g2s(smem_u32(stage + (size_t)rr * kN3Group * kN3CW * 16),
+                   A + (r0 + rr) * lda + v0 * V, bytes, fb);
+      }
+    }
+    return;
+  }
+
+  // ---- consumers: warp = chunk within the group
+  int64_t cur_g = -1;
+  double pv[kN3U][V];
+  bool live[kN3U];
+  for (int64_t u = u0, it = 0; u < u1; ++u, ++it) {
+    const int s = (int)(it % kN3Stages);
+    const int64_t round = it / kN3Stages;
+    const int64_t g = u / rows8, r0 = (u % rows8) * kN3Rows;
+    const int64_t chunk = g * kN3Group + warp;
+    if (g != cur_g) {  // this warp's slice of p (p = p_src / *p_scale)
+      cur_g = g;
+      const double scale = p_scale ? *p_scale : 1.0;
+#pragma unroll
+      for (int uu = 0; uu < kN3U; ++uu) {
+        const int64_t vi = chunk * kN3CW + uu * 32 + lane;
+        live[uu] = chunk < nchunks && vi < nvec;
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          const int64_t col = vi * V + k;
+          double x = (live[uu] && col < n_true) ? p_src[col] : 0.0;
+          if (p_scale) {
+            x = x / scale;
+            if (r0 == 0 && p_dst && live[uu] && col < n_true) p_dst[col] = x;
+          }
+          pv[uu][k] = x;
+        }
+      }
+    }
+    while (!mbar_try_wait(smem_u32(&full[s]), (uint32_t)(round & 1))) {
+    }
+    const TA* stage = reinterpret_cast<const TA*>(n3_smem + (size_t)s * kN3StageBytes);
+    double v[8];
+#pragma unroll
+    for (int rr = 0; rr < kN3Rows; ++rr) {
+      double acc = 0.0;
+      const TA* row = stage + (size_t)rr * kN3Group * kN3CW * V + (size_t)warp * kN3CW * V;
+#pragma unroll
+      for (int uu = 0; uu < kN3U; ++uu) {
+        if (live[uu] && r0 + rr < m) {
+          AVec<TA> a;
+          const TA* p = row + (uu * 32 + lane) * V;
+          if constexpr (V == 2) {
+            const double2 d = *reinterpret_cast<const double2*>(p);
+            a.v[0] = d.x;
+            a.v[1] = d.y;
+          } else {
+            const float4 f = *reinterpret_cast<const float4*>(p);
+            a.v[0] = f.x;
+            a.v[1] = f.y;
+            a.v[2] = f.z;
+            a.v[3] = f.w;
+          }
+#pragma unroll
+          for (int k = 0; k < V; ++k) acc = fma(a.get(k), pv[uu][k], acc);
+        }
+      }
+      v[rr] = acc;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&empty[s]));  // stage free for the producer
     const double t = warp_sum8(v);
-    const int64_t row = r + warp_sum8_index(lane);
-    if ((lane & 3) == 0 && row < r_end) part[(int64_t)chunk * m + row] = t;
+    const int64_t row = r0 + warp_sum8_index(lane);
+    if ((lane & 3) == 0 && row < m && chunk < nchunks) part[chunk * m + row] = t;
   }
 }
 
@@ -750,20 +923,6 @@ k_cgs2_coop(CgsCoopArgs a) {
 // of three times, and at full bulk-copy bandwidth instead of latency-bound
 // warp loads.  Used when the tile fits in shared memory (small / medium
 // bases: the L2-resident regime where CGS is latency-bound).
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      " selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-
 template <int MAXE>
 __global__ void __launch_bounds__(kThreads, 1)
 k_cgs2_tile(CgsCoopArgs a) {

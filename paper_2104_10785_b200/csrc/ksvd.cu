@@ -632,13 +632,32 @@ static double* Qcol(ksvd_run* R, int j) { return R->Q + (int64_t)j * R->ldq; }
 static double* Pcol(ksvd_run* R, int j) { return R->P + (int64_t)j * R->ldp; }
 
 // One GK iteration i (1-based), bidiag.py:151-178.
+// host-side enqueue timing per section (KSVD_DEBUG_HOST)
+static double g_tsec[6];
+struct SecTimer {
+  int k;
+  std::chrono::steady_clock::time_point t0;
+  explicit SecTimer(int k_) : k(k_), t0(std::chrono::steady_clock::now()) {}
+  ~SecTimer() {
+    g_tsec[k] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+};
+
 static int enqueue_step(ksvd_run* R, int i) {
   ksvd_mat* M = R->M;
   ksvd_ctx* c = M->ctx;
-  TRY(grow_bases(R, i + 1 <= R->k_max ? i + 1 : i));
+  {
+    SecTimer t(0);
+    TRY(grow_bases(R, i + 1 <= R->k_max ? i + 1 : i));
+  }
+  SecTimer t_all(5);
   // w = A p_i - alpha_i q_i, with p_i = z / alpha_i stored to P[:, i-1]
-  TRY(enqueue_gemv_n(M, R->z, R->alpha + i, Pcol(R, i - 1), Qcol(R, i - 1), R->alpha + i,
-                     R->w, R->st, i, /*finalize=*/!coop_enabled(c, i)));
+  {
+    SecTimer t(1);
+    TRY(enqueue_gemv_n(M, R->z, R->alpha + i, Pcol(R, i - 1), Qcol(R, i - 1), R->alpha + i,
+                       R->w, R->st, i, /*finalize=*/!coop_enabled(c, i)));
+  }
+  SecTimer t_cgs(2);
   // CGS2 against Q[:, :i]; beta_{i+1} = ||w||; beta < eps -> breakdown
   if (coop_enabled(c, i)) {
     FinArgs fin{M->part_n, M->mloc, M->mloc > 0 ? M->pn.nchunks : 0, R->alpha + i,
@@ -774,8 +793,10 @@ static int run_loop(ksvd_run* R, const double* q1_local) {
     CK(cudaMemsetAsync(c->tdbg, 0, sizeof t, c->stream));
   }
   if (dbg)
-    fprintf(stderr, "[ksvd] gk host: %d steps, enqueue %.3f ms, wait %.3f ms, launches %lld\n",
-            R->k_max, t_launch, t_wait, (long long)c->launches);
+    fprintf(stderr, "[ksvd] gk host: %d steps, enqueue %.3f ms (grow %.1f, gemv_n %.1f, "
+            "rest %.1f), wait %.3f ms, launches %lld\n", R->k_max, t_launch, g_tsec[0],
+            g_tsec[1], g_tsec[5] - g_tsec[1], t_wait, (long long)c->launches);
+  for (double& v : g_tsec) v = 0;
   return read_state(R);
 }
 

@@ -9,13 +9,13 @@
 #include "kernels.cuh"
 using namespace ksvd;
 
-template <typename TA, int U>
+template <typename TA, int U, int RB = 8>
 float time_n2(const TA* A, int64_t lda, int64_t m, int64_t n, const double* p, double* part,
               DevState* st, int sms, int ctas_per_sm) {
   constexpr int V = 16 / sizeof(TA);
   const int64_t nvec = (n + V - 1) / V;
   const int nchunks = (int)((nvec + 32 * U - 1) / (32 * U));
-  auto k = k_gemv_n2<TA, U>;
+  auto k = k_gemv_n2<TA, U, RB>;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, 0);
   const int per_sm = occ < ctas_per_sm ? occ : ctas_per_sm;
@@ -39,8 +39,38 @@ float time_n2(const TA* A, int64_t lda, int64_t m, int64_t n, const double* p, d
     cudaEventElapsedTime(&ms, a, b);
     best = ms < best ? ms : best;
   }
-  printf("  gemv_n2 U=%d occ=%d used=%d chunks=%d rows/warp=%lld: %8.1f us  %7.1f GB/s\n", U, occ,
+  printf("  gemv_n2 U=%d RB=%d occ=%d used=%d chunks=%d rows/warp=%lld: %8.1f us  %7.1f GB/s\n", U, RB, occ,
          per_sm, nchunks, (long long)rpw, 1e3 * best, m * n * sizeof(TA) / (best * 1e-3) / 1e9);
+  return best;
+}
+
+template <typename TA>
+float time_n3(const TA* A, int64_t lda, int64_t m, int64_t n, const double* p, double* part,
+              DevState* st, int sms) {
+  constexpr int V = 16 / sizeof(TA);
+  const int64_t nvec = (n + V - 1) / V;
+  const int nchunks = (int)((nvec + kN3CW - 1) / kN3CW);
+  const int64_t ngroups = (nchunks + kN3Group - 1) / kN3Group;
+  const int64_t rows8 = (m + kN3Rows - 1) / kN3Rows;
+  const int64_t units = ngroups * rows8;
+  auto k = k_gemv_n3<TA>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kN3Smem);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e9;
+  for (int r = 0; r < 10; ++r) {
+    cudaEventRecord(a);
+    k<<<sms, kN3Threads, kN3Smem>>>(A, lda, m, nvec, nchunks, rows8, units, p, nullptr, nullptr, n, part, st);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    best = ms < best ? ms : best;
+  }
+  printf("  gemv_n3 (TMA ring) chunks=%d groups=%lld: %8.1f us  %7.1f GB/s  [%s]\n", nchunks,
+         (long long)ngroups, 1e3 * best, m * n * sizeof(TA) / (best * 1e-3) / 1e9,
+         cudaGetErrorString(cudaGetLastError()));
   return best;
 }
 
@@ -94,11 +124,13 @@ void suite(int64_t m, int64_t n, int sms) {
   DevState* st;
   cudaMalloc(&st, sizeof(DevState));
   cudaMemset(st, 0, sizeof(DevState));
-  time_n2<TA, 1>(A, lda, m, n, p, part, st, sms, 8);
-  time_n2<TA, 2>(A, lda, m, n, p, part, st, sms, 8);
-  time_n2<TA, 4>(A, lda, m, n, p, part, st, sms, 8);
-  time_n2<TA, 2>(A, lda, m, n, p, part, st, sms, 4);
-  time_n2<TA, 4>(A, lda, m, n, p, part, st, sms, 2);
+  time_n3<TA>(A, lda, m, n, p, part, st, sms);
+  time_n2<TA, 1, 8>(A, lda, m, n, p, part, st, sms, 8);
+  time_n2<TA, 1, 16>(A, lda, m, n, p, part, st, sms, 8);
+  time_n2<TA, 1, 24>(A, lda, m, n, p, part, st, sms, 8);
+  time_n2<TA, 2, 8>(A, lda, m, n, p, part, st, sms, 8);
+  time_n2<TA, 2, 16>(A, lda, m, n, p, part, st, sms, 8);
+  time_n2<TA, 4, 8>(A, lda, m, n, p, part, st, sms, 8);
   timet<TA, 8, 1>(A, lda, m, n, w, part, st, sms, 8);
   timet<TA, 8, 8>(A, lda, m, n, w, part, st, sms, 8);
   timet<TA, 16, 8>(A, lda, m, n, w, part, st, sms, 8);
