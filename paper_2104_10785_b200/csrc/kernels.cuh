@@ -106,6 +106,23 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 
+// sum_{k < cnt} p[k*ld] with 8 loads in flight and 4 interleaved partial
+// sums combined in a fixed order (deterministic; not latency-chained)
+__device__ __forceinline__ double strided_sum(const double* __restrict__ p, int64_t ld,
+                                              int cnt) {
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  int k = 0;
+  for (; k + 8 <= cnt; k += 8) {
+    double t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t[u] = p[(int64_t)(k + u) * ld];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u & 3] += t[u];
+  }
+  for (; k < cnt; ++k) acc[k & 3] += p[(int64_t)k * ld];
+  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
 // ---------------------------------------------------------------------------
 // 16-byte streaming loads of A.  A is read exactly once per pass, so it is
 // loaded through the non-coherent path without L1 allocation.
@@ -153,7 +170,7 @@ __device__ __forceinline__ void flag_nonfinite(DevState* st, double v, int step)
 template <typename TA, int U, int RB = 8>
 __global__ void __launch_bounds__(kThreads)
 k_gemv_n2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nchunks,
-          int64_t rows_per_warp, const double* __restrict__ p_src,
+          int64_t nseg, const double* __restrict__ p_src,
           const double* __restrict__ p_scale, double* __restrict__ p_dst, int64_t n_true,
           double* __restrict__ part, const DevState* st) {
   static_assert(RB % 8 == 0, "rows per iteration: multiple of 8");
@@ -164,9 +181,7 @@ k_gemv_n2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nc
   const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const int chunk = (int)(gw % nchunks);
   const int64_t rseg = gw / nchunks;
-  const int64_t r_begin = rseg * rows_per_warp;
-  if (r_begin >= m) return;
-  const int64_t r_end = min(m, r_begin + rows_per_warp);
+  if (rseg >= nseg) return;
   const double scale = p_scale ? *p_scale : 1.0;
   double pv[U][V];
   bool live[U];
@@ -186,7 +201,10 @@ k_gemv_n2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nc
     }
   }
   const TA* base = A + ((int64_t)chunk * CW + lane) * V;
-  for (int64_t r = r_begin; r < r_end; r += RB) {
+  // row blocks rseg, rseg + nseg, ...: all warps move down the matrix as one
+  // band, so the rows read last stay in L2 for k_gemv_t, which sweeps up
+  for (int64_t r = rseg * RB; r < m; r += nseg * RB) {
+    const int64_t r_end = min(m, r + RB);
     AVec<TA> a[RB][U];
 #pragma unroll
     for (int rr = 0; rr < RB; ++rr) {
@@ -380,8 +398,7 @@ k_gemv_n_finalize(const double* __restrict__ part, int64_t part_ld, int nchunks,
   if (halted(st)) return;
   const int64_t r = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   if (r >= m) return;
-  double s = part[r];
-  for (int c = 1; c < nchunks; ++c) s += part[(int64_t)c * part_ld + r];
+  double s = strided_sum(part + r, part_ld, nchunks);
   if (qprev) s = s - (*alpha) * qprev[r];
   w[r] = s;
   flag_nonfinite(st, s, step);
@@ -404,26 +421,32 @@ constexpr int kQB = 1024;
 template <typename TA, int U, int RG>
 __global__ void __launch_bounds__(kThreads)
 k_gemv_t(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
-         int64_t rows_per_split, const double* __restrict__ q_src,
+         int64_t /*unused*/, const double* __restrict__ q_src,
          const double* __restrict__ q_scale, double* __restrict__ q_dst,
          double* __restrict__ part, int64_t ldz, const DevState* st) {
   if (halted(st)) return;
   constexpr int V = AVec<TA>::V;
   constexpr int TPG = kThreads / RG;
-  __shared__ double q_s[kQB];
+  constexpr int RBT = RG * U;  // rows per block: U rows in flight per group
+  static_assert(RBT <= kQB, "row block exceeds the q staging buffer");
+  __shared__ double q_s[RBT];
   __shared__ double red[RG > 1 ? RG : 1][RG > 1 ? TPG * V : 1];
   const int g = threadIdx.x / TPG, t = threadIdx.x % TPG;
   const int64_t vcol = (int64_t)blockIdx.x * TPG + t;
   const bool active = vcol < nvec;
-  const int64_t r0 = (int64_t)blockIdx.y * rows_per_split;
-  const int64_t r1 = min(m, r0 + rows_per_split);
+  const int64_t nsplit = gridDim.y, s = blockIdx.y;
+  const int64_t nblk = (m + RBT - 1) / RBT;
   const double scale = q_scale ? *q_scale : 1.0;
   double acc[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.0;
   const TA* base = A + vcol * V;
-  for (int64_t rb = r0; rb < r1; rb += kQB) {
-    const int nr = (int)min((int64_t)kQB, r1 - rb);
+  // row blocks s, s + nsplit, ... visited bottom-up: the grid sweeps A as a
+  // band from the last rows (still in L2 after k_gemv_n2) to the first
+  const int64_t last = s < nblk ? s + ((nblk - 1 - s) / nsplit) * nsplit : -1;
+  for (int64_t b = last; b >= 0; b -= nsplit) {
+    const int64_t rb = b * RBT;
+    const int nr = (int)min((int64_t)RBT, m - rb);
     __syncthreads();
     for (int e = threadIdx.x; e < nr; e += kThreads) {
       double qv = q_src[rb + e];
@@ -436,24 +459,24 @@ k_gemv_t(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
     __syncthreads();
     if (!active) continue;
     const TA* p = base + rb * lda;
-    int r = g;
-    for (; r + (U - 1) * RG < nr; r += U * RG) {
+    if (nr == RBT) {
       AVec<TA> a[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) a[u].load(p + (int64_t)(r + u * RG) * lda);
+      for (int u = 0; u < U; ++u) a[u].load(p + (int64_t)(g + u * RG) * lda);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const double qv = q_s[r + u * RG];
+        const double qv = q_s[g + u * RG];
 #pragma unroll
         for (int k = 0; k < V; ++k) acc[k] = fma(a[u].get(k), qv, acc[k]);
       }
-    }
-    for (; r < nr; r += RG) {
-      AVec<TA> a;
-      a.load(p + (int64_t)r * lda);
-      const double qv = q_s[r];
+    } else {
+      for (int r = g; r < nr; r += RG) {
+        AVec<TA> a;
+        a.load(p + (int64_t)r * lda);
+        const double qv = q_s[r];
 #pragma unroll
-      for (int k = 0; k < V; ++k) acc[k] = fma(a.get(k), qv, acc[k]);
+        for (int k = 0; k < V; ++k) acc[k] = fma(a.get(k), qv, acc[k]);
+      }
     }
   }
   if constexpr (RG > 1) {
@@ -463,10 +486,10 @@ k_gemv_t(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
     if (g == 0 && active) {
 #pragma unroll
       for (int k = 0; k < V; ++k) {
-        double s = red[0][t * V + k];
+        double sum = red[0][t * V + k];
 #pragma unroll
-        for (int gg = 1; gg < RG; ++gg) s += red[gg][t * V + k];
-        acc[k] = s;
+        for (int gg = 1; gg < RG; ++gg) sum += red[gg][t * V + k];
+        acc[k] = sum;
       }
     }
   }
@@ -783,8 +806,7 @@ k_cgs2_coop(CgsCoopArgs a) {
   // [0] finalisation of the split partial sums of A^T q
   if (a.fpart) {
     for (int64_t r = s0 + threadIdx.x; r < s1; r += kThreads) {
-      double v = 0.0;
-      for (int k = 0; k < a.fnsplit; ++k) v += a.fpart[(int64_t)k * a.fld + r];
+      double v = strided_sum(a.fpart + r, a.fld, a.fnsplit);
       if (a.fp) v = v - (*a.fbeta) * a.fp[r];
       a.x[r] = v;
       flag_nonfinite(a.st, v, a.step);
@@ -926,6 +948,9 @@ k_cgs2_coop(CgsCoopArgs a) {
 template <int MAXE>
 __global__ void __launch_bounds__(kThreads, 1)
 k_cgs2_tile(CgsCoopArgs a) {
+  unsigned long long t_entry = 0;
+  if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0)
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_entry));
   if (halted(a.st)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double tred[kWarps][32 * MAXE];
@@ -963,8 +988,7 @@ k_cgs2_tile(CgsCoopArgs a) {
   // [0] finalisation of the split partial sums of A^T q (overlaps the copy)
   if (a.fpart) {
     for (int64_t r = s0 + threadIdx.x; r < s1; r += kThreads) {
-      double v = 0.0;
-      for (int k = 0; k < a.fnsplit; ++k) v += a.fpart[(int64_t)k * a.fld + r];
+      double v = strided_sum(a.fpart + r, a.fld, a.fnsplit);
       if (a.fp) v = v - (*a.fbeta) * a.fp[r];
       a.x[r] = v;
       flag_nonfinite(a.st, v, a.step);
@@ -972,6 +996,7 @@ k_cgs2_tile(CgsCoopArgs a) {
   }
   unsigned long long tl = 0;
   phase_mark(a.tdbg, 0, tl);
+  if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(a.tdbg + 5, tl - t_entry);
   __syncthreads();
   // x rows of this CTA live in registers for the whole kernel (loaded while
   // the tile is in flight)
@@ -1092,6 +1117,12 @@ k_cgs2_tile(CgsCoopArgs a) {
                      : "memory");
       }
     }
+  }
+  if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    atomicAdd(a.tdbg + 6, now - t_entry);
+    atomicAdd(a.tdbg + 7, 1ull);
   }
 }
 
