@@ -966,17 +966,23 @@ k_cgs2_tile(CgsCoopArgs a) {
   double* cs = tile + (size_t)a.ncols * ldt;  // coefficients of the current pass
   const uint32_t bar = smem_u32(&mbar);
 
-  // bulk-async load of the basis tile (thread 0 issues, all wait later)
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  // bulk-async load of the basis tile: lane 0 of warp 0 arms the mbarrier
+  // with the total byte count, then the 32 lanes of warp 0 issue the
+  // per-column copies (one thread issuing ~100+ copies serially was the
+  // largest fixed cost of this kernel); all threads wait later.
+  if (warp == 0) {
     const uint32_t bytes = (uint32_t)ldt * 8u;
-    const uint32_t total = bytes * (uint32_t)a.ncols;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                 "r"(total)
-                 : "memory");
+    if (lane == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      const uint32_t total = bytes * (uint32_t)a.ncols;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                   "r"(total)
+                   : "memory");
+    }
+    __syncwarp();
     if (bytes)
-      for (int j = 0; j < a.ncols; ++j) {
+      for (int j = lane; j < a.ncols; j += 32) {
         const double* src = a.B + (int64_t)j * a.ldb + s0;
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
@@ -1172,57 +1178,133 @@ k_basis_combine(const double* __restrict__ P, int64_t ldp, int64_t n, int kp,
     if (t0 + tt < take) V[(int64_t)(t0 + tt) * ldv + r] = acc[tt];
 }
 
-// Y[:, t] = (A X[:, t]) / sigma[t] for a block of up to 32 right-hand sides:
-// one pass over A for all of them (the reference runs `take` separate
-// matvecs, fsvd.py:193-194).  CTA tile: kMR rows x 32 columns; lane = column,
-// each warp owns kMR/8 rows; A and X are staged through shared memory in
-// kKC-column slabs.
-constexpr int kMR = 64;
-constexpr int kKC = 32;
+// Y[:, t] = (A X[:, t]) / sigma[t] on the FP64 tensor cores (DMMA,
+// mma.sync.m8n8k4.f64): one pass over A for up to 32 right-hand sides per
+// CTA column (the reference runs `take` separate matvecs, fsvd.py:193-194).
+// CTA tile 256 rows x 32 columns, 8 warps x (32 rows x 32 columns) = 4 x 4
+// m8n8 accumulator tiles per warp.  A is staged in 32-column slabs with
+// cp.async (two-stage ring) into a padded row-major layout whose fragment
+// reads are bank-conflict-free (row stride = 4 mod 16 doubles / 4 mod 32
+// floats); X^T is staged the same way.  Per k-step of 4: 4 A-fragment and 4
+// B-fragment shared loads feed 16 DMMAs.  Deterministic (fixed k order).
+constexpr int kMR = 256, kMC = 32, kMKC = 32;
+constexpr int kMStride = kMKC + 4;  // padded row stride (elements)
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const uint32_t s = smem_u32(smem);
+  const int n = pred ? 16 : 0;  // src-size 0 -> zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+
 template <typename TA>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 2)
 k_multi_rhs(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t n,
             const double* __restrict__ X, int64_t ldx, int ncols,
-            const double* __restrict__ sigma, double* __restrict__ Y,
-            int64_t ldy) {
-  __shared__ double As[kMR][kKC + 1];
-  __shared__ double Xs[kKC][33];
+            const double* __restrict__ sigma, double* __restrict__ Y, int64_t ldy) {
+  constexpr int V = AVec<TA>::V;
+  constexpr int VPR = kMKC / V;                 // 16-byte vectors per slab row
+  constexpr int APER = kMR * VPR / kThreads;    // A vectors per thread per slab
+  extern __shared__ __align__(16) unsigned char mrhs_smem[];
+  TA* As = reinterpret_cast<TA*>(mrhs_smem);                      // [2][kMR][kMStride]
+  double* Xt = reinterpret_cast<double*>(As + 2 * kMR * kMStride);  // [2][kMC][kMStride]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t r0 = (int64_t)blockIdx.x * kMR;
-  const int t0 = blockIdx.y * 32;
-  constexpr int RW = kMR / kWarps;  // rows per warp
-  double acc[RW];
+  const int t0 = blockIdx.y * kMC;
+  const int64_t nvec = (n + V - 1) / V;
+  const int64_t nslab = (n + kMKC - 1) / kMKC;
+
+  auto stage = [&](int buf, int64_t k0) {
+    TA* as = As + (size_t)buf * kMR * kMStride;
 #pragma unroll
-  for (int i = 0; i < RW; ++i) acc[i] = 0.0;
-  for (int64_t k0 = 0; k0 < n; k0 += kKC) {
+    for (int q = 0; q < APER; ++q) {
+      const int e = tid + q * kThreads;
+      const int rr = e / VPR, vv = e % VPR;
+      const int64_t r = r0 + rr, vi = k0 / V + vv;
+      const bool ok = r < m && vi < nvec;
+      cp_async16(as + rr * kMStride + vv * V, ok ? (const void*)(A + r * lda + vi * V) : (const void*)A,
+                 ok);
+    }
+    double* xt = Xt + (size_t)buf * kMC * kMStride;
+    // X^T slab: column t, 32 k values (8 x 16 B per column)
+    for (int e = tid; e < kMC * (kMKC / 2); e += kThreads) {
+      const int tt = e / (kMKC / 2), vv = e % (kMKC / 2);
+      const int64_t k = k0 + 2 * vv;
+      const bool ok = t0 + tt < ncols && k + 1 < n;
+      if (ok || !(t0 + tt < ncols && k < n)) {
+        cp_async16(xt + tt * kMStride + 2 * vv,
+                   ok ? (const void*)(X + (int64_t)(t0 + tt) * ldx + k) : (const void*)X, ok);
+      } else {  // odd tail element
+        xt[tt * kMStride + 2 * vv] = X[(int64_t)(t0 + tt) * ldx + k];
+        xt[tt * kMStride + 2 * vv + 1] = 0.0;
+      }
+    }
+    cp_async_commit();
+  };
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int fr = lane >> 2, fk = lane & 3;  // fragment row / k index
+  stage(0, 0);
+  for (int64_t s = 0; s < nslab; ++s) {
+    const int buf = (int)(s & 1);
+    if (s + 1 < nslab) {
+      stage(buf ^ 1, (s + 1) * kMKC);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
     __syncthreads();
-    for (int e = tid; e < kMR * kKC; e += kThreads) {
-      const int rr = e / kKC, kk = e % kKC;
-      const int64_t r = r0 + rr, k = k0 + kk;
-      As[rr][kk] = (r < m && k < n) ? (double)A[r * lda + k] : 0.0;
-    }
-    for (int e = tid; e < kKC * 32; e += kThreads) {
-      const int kk = e % kKC, tt = e / kKC;
-      const int64_t k = k0 + kk;
-      Xs[kk][tt] = (k < n && t0 + tt < ncols) ? X[(int64_t)(t0 + tt) * ldx + k] : 0.0;
+    const TA* as = As + (size_t)buf * kMR * kMStride + (size_t)(warp * 32) * kMStride;
+    const double* xt = Xt + (size_t)buf * kMC * kMStride;
+#pragma unroll
+    for (int kb = 0; kb < kMKC; kb += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = (double)as[(i * 8 + fr) * kMStride + kb + fk];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = xt[(j * 8 + fr) * kMStride + kb + fk];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
     }
     __syncthreads();
-#pragma unroll 4
-    for (int kk = 0; kk < kKC; ++kk) {
-      const double xv = Xs[kk][lane];
-#pragma unroll
-      for (int i = 0; i < RW; ++i) acc[i] = fma(As[warp * RW + i][kk], xv, acc[i]);
-    }
   }
-  const int t = t0 + lane;
-  if (t < ncols) {
-    const double s = sigma ? sigma[t] : 1.0;
+  // D fragment: row fr, columns 2*fk, 2*fk+1 of each 8 x 8 tile
 #pragma unroll
-    for (int i = 0; i < RW; ++i) {
-      const int64_t r = r0 + warp * RW + i;
-      if (r < m) Y[(int64_t)t * ldy + r] = sigma ? acc[i] / s : acc[i];
-    }
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = r0 + warp * 32 + i * 8 + fr;
+    if (r >= m) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int t = t0 + j * 8 + 2 * fk + h;
+        if (t < ncols) Y[(int64_t)t * ldy + r] = sigma ? acc[i][j][h] / sigma[t] : acc[i][j][h];
+      }
   }
+}
+
+template <typename TA>
+constexpr size_t multi_rhs_smem() {
+  return 2 * (size_t)kMR * kMStride * sizeof(TA) + 2 * (size_t)kMC * kMStride * sizeof(double);
 }
 
 // fix_signs (linops.py:271-282): per column j, s = sign(V[argmax|V[:,j]|, j])

@@ -225,31 +225,46 @@ static int plan_matrix(ksvd_mat* M) {
   return 0;
 }
 
+// Leading dimension of A on the device: rows padded to a 16-byte multiple
+// only (what the 16-byte vector loads and bulk copies need), so a
+// contiguous host matrix uploads as ONE DMA.  KSVD_LDA_BYTES=512 restores
+// 512-byte row alignment (measured equivalent for the streaming kernels).
+static int64_t lda_for(int64_t n, int64_t es) {
+  static const int64_t align = [] {
+    const char* e = getenv("KSVD_LDA_BYTES");
+    const long v = e ? atol(e) : 16;
+    return (int64_t)(v >= 16 && (v & (v - 1)) == 0 ? v : 16);
+  }();
+  return rup(n, align / es);
+}
+
+// All matrix buffers come from the stream-ordered pool (no device-wide
+// synchronisation on allocation or free; the pool keeps its memory).
 static int alloc_matrix_buffers(ksvd_mat* M) {
+  cudaStream_t s = M->ctx->stream;
   const size_t abytes = (size_t)M->mloc * M->lda * esize(M->dtype);
-  CK(cudaMalloc(&M->A, std::max<size_t>(abytes, 16)));
+  CK(cudaMallocAsync(&M->A, std::max<size_t>(abytes, 16), s));
   TRY(plan_matrix(M));
-  CK(cudaMalloc(&M->part_n, sizeof(double) * M->pn.nchunks * std::max<int64_t>(M->mloc, 1)));
-  CK(cudaMalloc(&M->part_t, sizeof(double) * M->pt.nsplit * M->n_pad));
-  CK(cudaMalloc(&M->dx, sizeof(double) * std::max(M->n_pad, M->m_pad)));
-  CK(cudaMalloc(&M->dy, sizeof(double) * std::max(M->n_pad, M->m_pad)));
-  CK(cudaMemset(M->dx, 0, sizeof(double) * std::max(M->n_pad, M->m_pad)));
-  CK(cudaMemset(M->dy, 0, sizeof(double) * std::max(M->n_pad, M->m_pad)));
-  CK(cudaMalloc(&M->st0, sizeof(DevState)));
-  CK(cudaMemset(M->st0, 0, sizeof(DevState)));
+  const size_t vec = sizeof(double) * std::max(M->n_pad, M->m_pad);
+  CK(cudaMallocAsync((void**)&M->part_n,
+                     sizeof(double) * M->pn.nchunks * std::max<int64_t>(M->mloc, 1), s));
+  CK(cudaMallocAsync((void**)&M->part_t, sizeof(double) * M->pt.nsplit * M->n_pad, s));
+  CK(cudaMallocAsync((void**)&M->dx, vec, s));
+  CK(cudaMallocAsync((void**)&M->dy, vec, s));
+  CK(cudaMemsetAsync(M->dx, 0, vec, s));
+  CK(cudaMemsetAsync(M->dy, 0, vec, s));
+  CK(cudaMallocAsync((void**)&M->st0, sizeof(DevState), s));
+  CK(cudaMemsetAsync(M->st0, 0, sizeof(DevState), s));
   return 0;
 }
 
 static int free_matrix(ksvd_mat* M) {
   if (!M) return 0;
+  cudaStream_t s = M->ctx->stream;
   cudaSetDevice(M->ctx->device);
-  cudaStreamSynchronize(M->ctx->stream);
-  cudaFree(M->A);
-  cudaFree(M->part_n);
-  cudaFree(M->part_t);
-  cudaFree(M->dx);
-  cudaFree(M->dy);
-  cudaFree(M->st0);
+  for (void* p : {(void*)M->A, (void*)M->part_n, (void*)M->part_t, (void*)M->dx, (void*)M->dy,
+                  (void*)M->st0})
+    if (p) cudaFreeAsync(p, s);
   cudaFree(M->gen_ps);
   cudaFree(M->gen_q);
   delete M;
@@ -841,8 +856,14 @@ template <typename TA>
 static int enqueue_multi_rhs(ksvd_mat* M, const double* X, int64_t ldx, int k,
                              const double* sigma, double* Y, int64_t ldy) {
   if (M->mloc == 0 || k == 0) return 0;
-  dim3 grid((unsigned)cdiv(M->mloc, kMR), (unsigned)cdiv(k, 32));
-  return launch(M->ctx, KC_OTHER, k_multi_rhs<TA>, grid, dim3(kThreads), 0,
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_multi_rhs<TA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)multi_rhs_smem<TA>()));
+    attr = true;
+  }
+  dim3 grid((unsigned)cdiv(M->mloc, kMR), (unsigned)cdiv(k, kMC));
+  return launch(M->ctx, KC_OTHER, k_multi_rhs<TA>, grid, dim3(kThreads), multi_rhs_smem<TA>(),
                 (const TA*)M->A, M->lda, M->mloc, M->n, X, ldx, k, sigma, Y, ldy);
 }
 
@@ -1137,7 +1158,7 @@ static int matrix_new(ksvd_ctx* c, const void* rows, int64_t m, int64_t n, int64
   M->mloc = mloc;
   M->dtype = dtype;
   const int64_t es = (int64_t)esize(dtype);
-  M->lda = rup(n, 512 / es);
+  M->lda = lda_for(n, es);
   M->n_pad = rup(n, 64);
   M->m_pad = rup(std::max<int64_t>(mloc, 1), 64);
   int rc = alloc_matrix_buffers(M);
@@ -1153,8 +1174,11 @@ static int matrix_new(ksvd_ctx* c, const void* rows, int64_t m, int64_t n, int64
         return set_err(KSVD_ERUNTIME, "memset: %s", cudaGetErrorString(e));
       }
     }
-    cudaError_t e = cudaMemcpy2DAsync(M->A, (size_t)M->lda * es, rows, (size_t)src_ld * es,
-                                      (size_t)n * es, (size_t)mloc, kind, c->stream);
+    cudaError_t e =
+        (src_ld == n && M->lda == n)  // contiguous on both sides: one linear DMA
+            ? cudaMemcpyAsync(M->A, rows, (size_t)mloc * n * es, kind, c->stream)
+            : cudaMemcpy2DAsync(M->A, (size_t)M->lda * es, rows, (size_t)src_ld * es,
+                                (size_t)n * es, (size_t)mloc, kind, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) {
       free_matrix(M);
@@ -1195,7 +1219,7 @@ int ksvd_matrix_generate(ksvd_ctx* c, const ksvd_gen_spec* sp, ksvd_mat** out) {
   M->mloc = mloc;
   M->dtype = sp->dtype;
   const int64_t es = (int64_t)esize(sp->dtype);
-  M->lda = rup(sp->n, 512 / es);
+  M->lda = lda_for(sp->n, es);
   M->n_pad = rup(sp->n, 64);
   M->m_pad = rup(std::max<int64_t>(mloc, 1), 64);
   int rc = alloc_matrix_buffers(M);
@@ -1281,10 +1305,12 @@ int ksvd_matmat(ksvd_mat* M, const double* X, int k, double* Y) {
   CK(cudaSetDevice(c->device));
   if (k <= 0) return k == 0 ? 0 : set_err(KSVD_ECONFIG, "k = %d", k);
   double *dX = nullptr, *dY = nullptr;
-  CK(cudaMallocAsync(&dX, sizeof(double) * M->n * k, c->stream));
+  // X columns at a 512-byte pitch (16-byte aligned cp.async sources)
+  CK(cudaMallocAsync(&dX, sizeof(double) * M->n_pad * k, c->stream));
   CK(cudaMallocAsync(&dY, sizeof(double) * std::max<int64_t>(M->mloc, 1) * k, c->stream));
-  CK(cudaMemcpyAsync(dX, X, sizeof(double) * M->n * k, cudaMemcpyHostToDevice, c->stream));
-  int rc = multi_rhs(M, dX, M->n, k, nullptr, dY, M->mloc);
+  CK(cudaMemcpy2DAsync(dX, sizeof(double) * M->n_pad, X, sizeof(double) * M->n,
+                       sizeof(double) * M->n, k, cudaMemcpyHostToDevice, c->stream));
+  int rc = multi_rhs(M, dX, M->n_pad, k, nullptr, dY, M->mloc);
   if (!rc && M->mloc > 0) {
     cudaError_t e = cudaMemcpyAsync(Y, dY, sizeof(double) * M->mloc * k,
                                     cudaMemcpyDeviceToHost, c->stream);
