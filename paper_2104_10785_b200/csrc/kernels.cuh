@@ -167,7 +167,7 @@ __device__ __forceinline__ void flag_nonfinite(DevState* st, double v, int step)
 // of the same rows, so a CTA reads long contiguous row segments.  Partials
 // per (chunk, row) go to part[chunk*m + row]; k_gemv_n_finalize adds them
 // in chunk order and applies - alpha q.
-template <typename TA, int U, int RB = 8>
+template <typename TA, int U, int RB = 8, int PF = 0>
 __global__ void __launch_bounds__(kThreads)
 k_gemv_n2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nchunks,
           int64_t nseg, const double* __restrict__ p_src,
@@ -202,9 +202,22 @@ k_gemv_n2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nc
   }
   const TA* base = A + ((int64_t)chunk * CW + lane) * V;
   // row blocks rseg, rseg + nseg, ...: all warps move down the matrix as one
-  // band, so the rows read last stay in L2 for k_gemv_t, which sweeps up
+  // band, so the rows read last stay in L2 for k_gemv_t, which sweeps up.
+  // Lanes 0..RB-1 also issue bulk L2 prefetches (cp.async.bulk.prefetch) of
+  // this warp's chunk of the rows PF iterations ahead: memory-level
+  // parallelism without holding registers for it.
+  const int64_t pf_vecs = nvec - (int64_t)chunk * CW < CW ? nvec - (int64_t)chunk * CW : (int64_t)CW;
+  const uint32_t pf_bytes = (uint32_t)(pf_vecs * 16);
+  const TA* pf_base = A + (int64_t)chunk * CW * V;
   for (int64_t r = rseg * RB; r < m; r += nseg * RB) {
     const int64_t r_end = min(m, r + RB);
+    if (PF > 0 && lane < RB) {
+      const int64_t rp = r + (int64_t)PF * nseg * RB + lane;
+      if (rp < m)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf_base + rp * lda),
+                     "r"(pf_bytes)
+                     : "memory");
+    }
     AVec<TA> a[RB][U];
 #pragma unroll
     for (int rr = 0; rr < RB; ++rr) {
@@ -421,29 +434,107 @@ constexpr int kQB = 1024;
 template <typename TA, int U, int RG>
 __global__ void __launch_bounds__(kThreads)
 k_gemv_t(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
-         int64_t /*unused*/, const double* __restrict__ q_src,
+         int64_t rows_per_split, const double* __restrict__ q_src,
          const double* __restrict__ q_scale, double* __restrict__ q_dst,
          double* __restrict__ part, int64_t ldz, const DevState* st) {
   if (halted(st)) return;
   constexpr int V = AVec<TA>::V;
   constexpr int TPG = kThreads / RG;
-  constexpr int RBT = RG * U;  // rows per block: U rows in flight per group
+  __shared__ double q_s[kQB];
+  __shared__ double red[RG > 1 ? RG : 1][RG > 1 ? TPG * V : 1];
+  const int g = threadIdx.x / TPG, t = threadIdx.x % TPG;
+  const int64_t vcol = (int64_t)blockIdx.x * TPG + t;
+  const bool active = vcol < nvec;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_split;
+  const int64_t r1 = min(m, r0 + rows_per_split);
+  const double scale = q_scale ? *q_scale : 1.0;
+  double acc[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) acc[k] = 0.0;
+  const TA* base = A + vcol * V;
+  for (int64_t rb = r0; rb < r1; rb += kQB) {
+    const int nr = (int)min((int64_t)kQB, r1 - rb);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr; e += kThreads) {
+      double qv = q_src[rb + e];
+      if (q_scale) {
+        qv = qv / scale;
+        if (blockIdx.x == 0 && q_dst) q_dst[rb + e] = qv;
+      }
+      q_s[e] = qv;
+    }
+    __syncthreads();
+    if (!active) continue;
+    const TA* p = base + rb * lda;
+    int r = g;
+    for (; r + (U - 1) * RG < nr; r += U * RG) {
+      AVec<TA> a[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) a[u].load(p + (int64_t)(r + u * RG) * lda);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double qv = q_s[r + u * RG];
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[k] = fma(a[u].get(k), qv, acc[k]);
+      }
+    }
+    for (; r < nr; r += RG) {
+      AVec<TA> a;
+      a.load(p + (int64_t)r * lda);
+      const double qv = q_s[r];
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] = fma(a.get(k), qv, acc[k]);
+    }
+  }
+  if constexpr (RG > 1) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) red[g][t * V + k] = acc[k];
+    __syncthreads();
+    if (g == 0 && active) {
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        double s = red[0][t * V + k];
+#pragma unroll
+        for (int gg = 1; gg < RG; ++gg) s += red[gg][t * V + k];
+        acc[k] = s;
+      }
+    }
+  }
+  if (g == 0 && active) {
+    double* dst = part + (int64_t)blockIdx.y * ldz + vcol * V;
+#pragma unroll
+    for (int k = 0; k < V; ++k) dst[k] = acc[k];
+  }
+}
+
+// k_gemv_t with the row blocks of its split interleaved across the splits
+// and visited bottom-up (block = RG*U*IT rows; CTA s takes blocks s,
+// s + nsplit, ... from the last one): the whole grid then sweeps A upwards as
+// one band, starting on the rows k_gemv_n2 (top-down band) left in L2.
+template <typename TA, int U, int RG, int IT>
+__global__ void __launch_bounds__(kThreads)
+k_gemv_t2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
+          int64_t /*unused*/, const double* __restrict__ q_src,
+          const double* __restrict__ q_scale, double* __restrict__ q_dst,
+          double* __restrict__ part, int64_t ldz, const DevState* st) {
+  if (halted(st)) return;
+  constexpr int V = AVec<TA>::V;
+  constexpr int TPG = kThreads / RG;
+  constexpr int RBT = RG * U * IT;
   static_assert(RBT <= kQB, "row block exceeds the q staging buffer");
   __shared__ double q_s[RBT];
   __shared__ double red[RG > 1 ? RG : 1][RG > 1 ? TPG * V : 1];
   const int g = threadIdx.x / TPG, t = threadIdx.x % TPG;
   const int64_t vcol = (int64_t)blockIdx.x * TPG + t;
   const bool active = vcol < nvec;
-  const int64_t nsplit = gridDim.y, s = blockIdx.y;
+  const int64_t nsplit = gridDim.y, sp = blockIdx.y;
   const int64_t nblk = (m + RBT - 1) / RBT;
   const double scale = q_scale ? *q_scale : 1.0;
   double acc[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.0;
   const TA* base = A + vcol * V;
-  // row blocks s, s + nsplit, ... visited bottom-up: the grid sweeps A as a
-  // band from the last rows (still in L2 after k_gemv_n2) to the first
-  const int64_t last = s < nblk ? s + ((nblk - 1 - s) / nsplit) * nsplit : -1;
+  const int64_t last = sp < nblk ? sp + ((nblk - 1 - sp) / nsplit) * nsplit : -1;
   for (int64_t b = last; b >= 0; b -= nsplit) {
     const int64_t rb = b * RBT;
     const int nr = (int)min((int64_t)RBT, m - rb);
@@ -459,24 +550,24 @@ k_gemv_t(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
     __syncthreads();
     if (!active) continue;
     const TA* p = base + rb * lda;
-    if (nr == RBT) {
+    int r = g;
+    for (; r + (U - 1) * RG < nr; r += U * RG) {
       AVec<TA> a[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) a[u].load(p + (int64_t)(g + u * RG) * lda);
+      for (int u = 0; u < U; ++u) a[u].load(p + (int64_t)(r + u * RG) * lda);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const double qv = q_s[g + u * RG];
+        const double qv = q_s[r + u * RG];
 #pragma unroll
         for (int k = 0; k < V; ++k) acc[k] = fma(a[u].get(k), qv, acc[k]);
       }
-    } else {
-      for (int r = g; r < nr; r += RG) {
-        AVec<TA> a;
-        a.load(p + (int64_t)r * lda);
-        const double qv = q_s[r];
+    }
+    for (; r < nr; r += RG) {
+      AVec<TA> a;
+      a.load(p + (int64_t)r * lda);
+      const double qv = q_s[r];
 #pragma unroll
-        for (int k = 0; k < V; ++k) acc[k] = fma(a.get(k), qv, acc[k]);
-      }
+      for (int k = 0; k < V; ++k) acc[k] = fma(a.get(k), qv, acc[k]);
     }
   }
   if constexpr (RG > 1) {

@@ -303,6 +303,19 @@ static int launch_gemv_t(ksvd_mat* M, dim3 grid, const double* q_src, const doub
                          double* q_dst, DevState* st) {
   ksvd_ctx* c = M->ctx;
   const GemvTPlan& pt = M->pt;
+  // band-ordered variant (k_gemv_t2): 256-row blocks when A is within a few
+  // L2 capacities (the band starts on what k_gemv_n2 left in L2), 1024-row
+  // blocks otherwise (same access granularity as contiguous splits)
+  const size_t abytes = (size_t)M->mloc * M->lda * esize(M->dtype);
+  if (pt.rg == 8) {
+    if (abytes < ((size_t)2 << 30))
+      return launch(c, KC_GEMV_T, k_gemv_t2<TA, kUnrollT, 8, 2>, grid, dim3(kThreads), 0,
+                    (const TA*)M->A, M->lda, M->mloc, M->pn.nvec, pt.rows_per_split, q_src,
+                    q_scale, q_dst, M->part_t, M->n_pad, (const DevState*)st);
+    return launch(c, KC_GEMV_T, k_gemv_t2<TA, kUnrollT, 8, 8>, grid, dim3(kThreads), 0,
+                  (const TA*)M->A, M->lda, M->mloc, M->pn.nvec, pt.rows_per_split, q_src,
+                  q_scale, q_dst, M->part_t, M->n_pad, (const DevState*)st);
+  }
 #define KSVD_GT(RG)                                                                    \
   launch(c, KC_GEMV_T, k_gemv_t<TA, kUnrollT, RG>, grid, dim3(kThreads), 0,             \
          (const TA*)M->A, M->lda, M->mloc, M->pn.nvec, pt.rows_per_split, q_src, q_scale, \
@@ -310,8 +323,7 @@ static int launch_gemv_t(ksvd_mat* M, dim3 grid, const double* q_src, const doub
   switch (pt.rg) {
     case 1: return KSVD_GT(1);
     case 2: return KSVD_GT(2);
-    case 4: return KSVD_GT(4);
-    default: return KSVD_GT(8);
+    default: return KSVD_GT(4);
   }
 #undef KSVD_GT
 }

@@ -9,22 +9,20 @@
 #include "kernels.cuh"
 using namespace ksvd;
 
-template <typename TA, int U, int RB = 8>
+template <typename TA, int U, int RB = 8, int PF = 0>
 float time_n2(const TA* A, int64_t lda, int64_t m, int64_t n, const double* p, double* part,
               DevState* st, int sms, int ctas_per_sm) {
   constexpr int V = 16 / sizeof(TA);
   const int64_t nvec = (n + V - 1) / V;
   const int nchunks = (int)((nvec + 32 * U - 1) / (32 * U));
-  auto k = k_gemv_n2<TA, U, RB>;
+  auto k = k_gemv_n2<TA, U, RB, PF>;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, 0);
   const int per_sm = occ < ctas_per_sm ? occ : ctas_per_sm;
   const int64_t warps = (int64_t)sms * per_sm * 8;
   int64_t rsegs = warps / nchunks;
   if (rsegs < 1) rsegs = 1;
-  int64_t rpw = (m + rsegs - 1) / rsegs;
-  rpw = (rpw + 7) / 8 * 8;
-  rsegs = (m + rpw - 1) / rpw;
+  const int64_t rpw = rsegs;  // nseg of the band-interleaved kernel
   const int64_t blocks = (rsegs * nchunks + 7) / 8;
   cudaEvent_t a, b;
   cudaEventCreate(&a);
@@ -39,7 +37,7 @@ float time_n2(const TA* A, int64_t lda, int64_t m, int64_t n, const double* p, d
     cudaEventElapsedTime(&ms, a, b);
     best = ms < best ? ms : best;
   }
-  printf("  gemv_n2 U=%d RB=%d occ=%d used=%d chunks=%d rows/warp=%lld: %8.1f us  %7.1f GB/s\n", U, RB, occ,
+  printf("  gemv_n2 PF=%d U=%d RB=%d occ=%d used=%d chunks=%d rows/warp=%lld: %8.1f us  %7.1f GB/s\n", PF, U, RB, occ,
          per_sm, nchunks, (long long)rpw, 1e3 * best, m * n * sizeof(TA) / (best * 1e-3) / 1e9);
   return best;
 }
@@ -71,6 +69,34 @@ float time_n3(const TA* A, int64_t lda, int64_t m, int64_t n, const double* p, d
   printf("  gemv_n3 (TMA ring) chunks=%d groups=%lld: %8.1f us  %7.1f GB/s  [%s]\n", nchunks,
          (long long)ngroups, 1e3 * best, m * n * sizeof(TA) / (best * 1e-3) / 1e9,
          cudaGetErrorString(cudaGetLastError()));
+  return best;
+}
+
+template <typename TA, int U, int RG, int IT>
+float timet2(const TA* A, int64_t lda, int64_t m, int64_t n, const double* q, double* part,
+             DevState* st, int sms, int target_per_sm) {
+  constexpr int V = 16 / sizeof(TA);
+  const int64_t nvec = (n + V - 1) / V;
+  const int64_t tiles = (nvec + 256 / RG - 1) / (256 / RG);
+  int64_t nsplit = ((int64_t)sms * target_per_sm + tiles - 1) / tiles;
+  if (nsplit < 1) nsplit = 1;
+  const int64_t ldz = (n + 63) / 64 * 64;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e9;
+  for (int r = 0; r < 10; ++r) {
+    cudaEventRecord(a);
+    k_gemv_t2<TA, U, RG, IT><<<dim3(tiles, nsplit), 256>>>(A, lda, m, nvec, 0, q, nullptr, nullptr,
+                                                          part, ldz, st);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    best = ms < best ? ms : best;
+  }
+  printf("  gemv_t2 U=%d RG=%d IT=%d ctas/sm=%d nsplit=%lld: %8.1f us  %7.1f GB/s\n", U, RG, IT,
+         target_per_sm, (long long)nsplit, 1e3 * best, m * n * sizeof(TA) / (best * 1e-3) / 1e9);
   return best;
 }
 
@@ -124,19 +150,14 @@ void suite(int64_t m, int64_t n, int sms) {
   DevState* st;
   cudaMalloc(&st, sizeof(DevState));
   cudaMemset(st, 0, sizeof(DevState));
-  time_n3<TA>(A, lda, m, n, p, part, st, sms);
-  time_n2<TA, 1, 8>(A, lda, m, n, p, part, st, sms, 8);
-  time_n2<TA, 1, 16>(A, lda, m, n, p, part, st, sms, 8);
-  time_n2<TA, 1, 24>(A, lda, m, n, p, part, st, sms, 8);
-  time_n2<TA, 2, 8>(A, lda, m, n, p, part, st, sms, 8);
-  time_n2<TA, 2, 16>(A, lda, m, n, p, part, st, sms, 8);
-  time_n2<TA, 4, 8>(A, lda, m, n, p, part, st, sms, 8);
-  timet<TA, 8, 1>(A, lda, m, n, w, part, st, sms, 8);
-  timet<TA, 8, 8>(A, lda, m, n, w, part, st, sms, 8);
-  timet<TA, 16, 8>(A, lda, m, n, w, part, st, sms, 8);
-  timet<TA, 8, 4>(A, lda, m, n, w, part, st, sms, 8);
-  timet<TA, 8, 8>(A, lda, m, n, w, part, st, sms, 4);
+  time_n2<TA, 4, 8, 0>(A, lda, m, n, p, part, st, sms, 8);
+  time_n2<TA, 2, 8, 0>(A, lda, m, n, p, part, st, sms, 8);
   timet<TA, 16, 8>(A, lda, m, n, w, part, st, sms, 4);
+  timet2<TA, 16, 8, 1>(A, lda, m, n, w, part, st, sms, 4);
+  timet2<TA, 16, 8, 2>(A, lda, m, n, w, part, st, sms, 4);
+  timet2<TA, 16, 8, 8>(A, lda, m, n, w, part, st, sms, 4);
+  timet2<TA, 16, 8, 2>(A, lda, m, n, w, part, st, sms, 8);
+  timet2<TA, 8, 8, 4>(A, lda, m, n, w, part, st, sms, 4);
   cudaFree(A);
   cudaFree(p);
   cudaFree(w);

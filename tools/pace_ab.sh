@@ -1,3 +1,3 @@
 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -x > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
-python tools/one_call.py --config 3 --calls 1 > gpurun_out/plain_c3.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_multi_rhs --csv --log-file gpurun_out/launches_mrhs3.csv python tools/one_call.py --config 3 --calls 1 > gpurun_out/ncu3.log 2>&1
-python tools/one_call.py --config 4 --calls 1 > gpurun_out/plain_c4.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_multi_rhs --csv --log-file gpurun_out/launches_mrhs4.csv python tools/one_call.py --config 4 --calls 1 > gpurun_out/ncu4.log 2>&1
+timeout 900 python bench.py --config 4 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
+timeout 600 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/bench.log 2>&1
