@@ -457,12 +457,28 @@ struct FinArgs {  // deferred gemv_t finalisation (phase 0 of k_cgs2_coop)
   const double* p = nullptr;
 };
 
-static bool coop_enabled(const ksvd_ctx* c, int ncols) {
+constexpr size_t kTileSmemMax = 200 * 1024;  // basis tile budget of k_cgs2_tile
+
+// Fused single-kernel CGS2 is used where its basis tile fits in shared
+// memory (one CTA per SM): there it beats the multi-kernel path by its
+// launches; for long vectors (configs 3-5, left side) the multi-kernel path
+// with ~L/128 CTAs streams the basis faster than a one-wave cooperative grid
+// (measured: config 3 581 vs 600 ms per call).  KSVD_COOP=0 disables the
+// fused path, KSVD_COOP_GLOBAL=1 also uses the streaming cooperative kernel.
+static bool coop_enabled(const ksvd_ctx* c, int64_t L, int ncols) {
   static const bool off = [] {
     const char* e = getenv("KSVD_COOP");
     return e && strcmp(e, "0") == 0;
   }();
-  return !off && c->comm == nullptr && ncols <= kCoopMaxCols;
+  static const bool global = [] {
+    const char* e = getenv("KSVD_COOP_GLOBAL");
+    return e && strcmp(e, "1") == 0;
+  }();
+  if (off || c->comm != nullptr || ncols > kCoopMaxCols) return false;
+  const int64_t G = std::min<int64_t>(c->sms, std::max<int64_t>(1, cdiv(L, 32)));
+  const int64_t rows = rup(cdiv(std::max<int64_t>(L, 1), G), 2);
+  const bool tile = rows <= 256 && sizeof(double) * (size_t)ncols * (size_t)(rows + 1) <= kTileSmemMax;
+  return tile || global;
 }
 
 static int coop_max_ctas(ksvd_ctx* c) {
@@ -477,8 +493,6 @@ static int coop_max_ctas(ksvd_ctx* c) {
   }
   return per_sm * c->sms;
 }
-
-constexpr size_t kTileSmemMax = 200 * 1024;  // basis tile budget of k_cgs2_tile
 
 template <int MAXE>
 static int tile_attr() {
@@ -683,11 +697,11 @@ static int enqueue_step(ksvd_run* R, int i) {
   {
     SecTimer t(1);
     TRY(enqueue_gemv_n(M, R->z, R->alpha + i, Pcol(R, i - 1), Qcol(R, i - 1), R->alpha + i,
-                       R->w, R->st, i, /*finalize=*/!coop_enabled(c, i)));
+                       R->w, R->st, i, /*finalize=*/!coop_enabled(c, M->mloc, i)));
   }
   SecTimer t_cgs(2);
   // CGS2 against Q[:, :i]; beta_{i+1} = ||w||; beta < eps -> breakdown
-  if (coop_enabled(c, i)) {
+  if (coop_enabled(c, M->mloc, i)) {
     FinArgs fin{M->part_n, M->mloc, M->mloc > 0 ? M->pn.nchunks : 0, R->alpha + i,
                 Qcol(R, i - 1)};
     TRY(cgs_coop(c, &R->left, R->Q, R->ldq, i, R->w, M->mloc, R->reorth, R->eps,
@@ -705,7 +719,7 @@ static int enqueue_step(ksvd_run* R, int i) {
   }
   // z = A^T q_{i+1} - beta_{i+1} p_i, q_{i+1} = w / beta stored to Q[:, i];
   // then CGS2 against P[:, :i] (replicated, no collective); alpha_{i+1} = ||z||
-  if (coop_enabled(c, i)) {
+  if (coop_enabled(c, M->n, i)) {
     TRY(enqueue_gemv_t(M, R->w, R->beta + i + 1, Qcol(R, i), R->beta + i + 1, Pcol(R, i - 1),
                        R->z, R->st, i, true, /*finalize=*/false));
     FinArgs fin{M->part_t, M->n_pad, M->mloc > 0 ? (int)M->pt.nsplit : 0, R->beta + i + 1,

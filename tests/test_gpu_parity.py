@@ -277,7 +277,8 @@ print(json.dumps(out))
 """
 
 
-@pytest.mark.parametrize("env", [{"KSVD_TILE": "0"}, {"KSVD_COOP": "0"}, {"KSVD_FORCE_NCCL": "1"}, {}])
+@pytest.mark.parametrize("env", [{"KSVD_TILE": "0"}, {"KSVD_COOP": "0"}, {"KSVD_FORCE_NCCL": "1"},
+                                 {"KSVD_COOP_GLOBAL": "1", "KSVD_TILE": "0"}, {}])
 def test_cgs_paths_agree(env):
     """The tile-resident, global-load cooperative and multi-kernel CGS2
     paths (selected at load time) all meet the parity bar; KSVD_FORCE_NCCL
