@@ -174,6 +174,18 @@ int ksvd_matrix_generate(ksvd_ctx *ctx, const ksvd_gen_spec *spec, ksvd_mat **ou
  * row-major); r receives the rank.  Either pointer may be NULL. */
 int ksvd_matrix_gen_factors(ksvd_mat *mat, double *Ps_local, double *Q, int *r);
 
+/* ---- KLRM snapshots (reference matrixio.py:15-46) ------------------------
+ * Little-endian header "<4sIQQ" (magic KLRM, u32 version 1, u64 rows, u64
+ * cols) + rows*cols f64 row-major payload.  The reader streams this rank's
+ * row shard straight into HBM through two pinned chunk buffers (file reads
+ * overlap the host-to-device copies; the payload never exists whole in host
+ * memory); dtype selects the device storage (KSVD_F32 rounds on the device).
+ * The writer streams the local rows back at their file offsets (rank 0 also
+ * writes the header), so N ranks write one file.  Format errors ->
+ * KSVD_ECONFIG with the reference's messages. */
+int ksvd_matrix_from_klrm(ksvd_ctx *ctx, const char *path, int dtype, ksvd_mat **out);
+int ksvd_matrix_to_klrm(ksvd_mat *mat, const char *path);
+
 /* ---- host spectral stage ------------------------------------------------
  * All eigenpairs of the symmetric tridiagonal (d, e), descending
  * (fsvd.py:63-134, implicit-shift QL, deflation |e| <= eps(|d_m|+|d_m+1|),

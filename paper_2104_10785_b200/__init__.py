@@ -13,6 +13,8 @@ from .errors import ConfigError, NumericalError, ShapeMismatchError
 from .fsvd import SymTridiag, fsvd, gram_tridiag, symtridiag_eig
 from .linops import (GK_START, DeviceMatrix, LinearOperator, PartialSvd,
                      as_operator, row_partition, substream)
+from .matrixio import (read_csv_matrix, read_matrix, read_matrix_device, write_matrix,
+                       write_matrix_device)
 from .rank import RankReport, count_above, estimate_rank
 
 __version__ = "0.1.0"
@@ -25,5 +27,6 @@ __all__ = [
     "GK_START", "DeviceMatrix", "LinearOperator", "PartialSvd", "as_operator",
     "row_partition", "substream",
     "RankReport", "count_above", "estimate_rank",
+    "read_csv_matrix", "read_matrix", "read_matrix_device", "write_matrix", "write_matrix_device",
     "__version__",
 ]

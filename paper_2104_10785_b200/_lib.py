@@ -76,6 +76,8 @@ SIGNATURES = {
     "ksvd_bidiag_sv2": (C.c_int, [C.c_int, _pd, _pd, _pd]),
     "ksvd_matrix_generate": (C.c_int, [_vp, C.POINTER(GenSpec), C.POINTER(_vp)]),
     "ksvd_matrix_gen_factors": (C.c_int, [_vp, _pd, _pd, _pi]),
+    "ksvd_matrix_from_klrm": (C.c_int, [_vp, C.c_char_p, C.c_int, C.POINTER(_vp)]),
+    "ksvd_matrix_to_klrm": (C.c_int, [_vp, C.c_char_p]),
 }
 
 _lib = None

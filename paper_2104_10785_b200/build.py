@@ -20,7 +20,8 @@ CSRC = HERE / "csrc"
 INCLUDE = ROOT / "include"
 LIB = HERE / "libksvd.so"
 SOURCES = [CSRC / "ksvd.cu", CSRC / "eig.cpp"]
-HEADERS = [CSRC / "kernels.cuh", INCLUDE / "ksvd.h"]
+HEADERS = [CSRC / "kernels.cuh", CSRC / "gen.cuh", CSRC / "klrm.cuh", INCLUDE / "ksvd.h",
+           INCLUDE / "ksvd_gen.h"]
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 
@@ -62,7 +63,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         f"-I{INCLUDE}", f"-I{CSRC}", f"-I{inc}",
         *[str(s) for s in SOURCES],
         "-o", str(tmp),
-        f"-L{lib}", "-l:libnccl.so.2", f"-Xlinker=-rpath,{lib}",
+        f"-L{lib}", "-l:libnccl.so.2", "-lpthread", f"-Xlinker=-rpath,{lib}",
     ]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)

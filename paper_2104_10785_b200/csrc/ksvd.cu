@@ -22,10 +22,12 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "gen.cuh"
 #include "kernels.cuh"
+#include "klrm.cuh"
 #include "ksvd.h"
 
 using namespace ksvd;
@@ -1029,6 +1031,168 @@ static int generate_into(ksvd_mat* M, const ksvd_gen_spec* sp) {
   return 0;
 }
 
+
+// ---------------------------------------------------------------------------
+// KLRM snapshots (reference matrixio.py:15-46)
+struct KlrmHeader {
+  char magic[4];
+  uint32_t version;
+  uint64_t rows, cols;
+};
+static_assert(sizeof(KlrmHeader) == 24, "KLRM header is <4sIQQ");
+
+static int64_t io_chunk_bytes() {
+  static const int64_t v = [] {
+    const char* e = getenv("KSVD_IO_CHUNK_BYTES");
+    const long long b = e ? atoll(e) : (64ll << 20);
+    return (int64_t)std::max(4096ll, b);
+  }();
+  return v;
+}
+
+static bool pread_all(int fd, void* buf, size_t bytes, off_t off) {
+  char* p = static_cast<char*>(buf);
+  while (bytes) {
+    const ssize_t r = pread(fd, p, bytes, off);
+    if (r <= 0) return false;
+    p += r;
+    bytes -= (size_t)r;
+    off += r;
+  }
+  return true;
+}
+// Page-cache copies are bound by one core's memcpy (~6 GB/s); split each
+// chunk across io threads (KSVD_IO_THREADS, default min(8, cores)).
+static int io_threads() {
+  static const int v = [] {
+    const char* e = getenv("KSVD_IO_THREADS");
+    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    return std::max(1, e ? atoi(e) : std::min(8, hw));
+  }();
+  return v;
+}
+template <class F>
+static bool io_parallel(size_t bytes, F&& part) {
+  const size_t grain = 1 << 20;
+  const int T = (int)std::min<size_t>((size_t)io_threads(), (bytes + grain - 1) / grain);
+  if (T <= 1) return part((size_t)0, bytes);
+  const size_t step = ((bytes + T - 1) / T + 4095) & ~(size_t)4095;
+  std::vector<std::thread> th;
+  std::vector<char> ok(T, 0);
+  for (int t = 0; t < T; ++t) {
+    const size_t lo = std::min(bytes, (size_t)t * step), hi = std::min(bytes, lo + step);
+    th.emplace_back([&, t, lo, hi] { ok[t] = part(lo, hi - lo); });
+  }
+  for (auto& x : th) x.join();
+  for (char o : ok)
+    if (!o) return false;
+  return true;
+}
+static bool pwrite_all(int fd, const void* buf, size_t bytes, off_t off) {
+  const char* p = static_cast<const char*>(buf);
+  while (bytes) {
+    const ssize_t r = pwrite(fd, p, bytes, off);
+    if (r <= 0) return false;
+    p += r;
+    bytes -= (size_t)r;
+    off += r;
+  }
+  return true;
+}
+
+// Pinned double buffer + device staging for chunked transfers.
+struct IoBuffers {
+  void* host[2] = {nullptr, nullptr};
+  double* dev = nullptr;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  ~IoBuffers() {
+    for (int b = 0; b < 2; ++b) {
+      if (host[b]) cudaFreeHost(host[b]);
+      if (ev[b]) cudaEventDestroy(ev[b]);
+    }
+    if (dev) cudaFree(dev);
+  }
+};
+
+static int klrm_read_into(ksvd_mat* M, int fd) {
+  ksvd_ctx* c = M->ctx;
+  cudaStream_t s = c->stream;
+  const int64_t n = M->n, mloc = M->mloc;
+  if (mloc == 0) return 0;
+  const int64_t rowb = n * 8;
+  const int64_t rpc = std::max<int64_t>(1, io_chunk_bytes() / rowb);  // rows per chunk
+  const size_t cbytes = (size_t)rpc * rowb;
+  IoBuffers io;
+  for (int b = 0; b < 2; ++b) {
+    CK(cudaHostAlloc(&io.host[b], cbytes, cudaHostAllocDefault));
+    CK(cudaEventCreateWithFlags(&io.ev[b], cudaEventDisableTiming));
+  }
+  if (M->dtype == KSVD_F32) CK(cudaMalloc((void**)&io.dev, cbytes));
+  const size_t es = esize(M->dtype);
+  int k = 0;
+  for (int64_t r = 0; r < mloc; r += rpc, ++k) {
+    const int b = k & 1;
+    const int64_t nr = std::min(rpc, mloc - r);
+    if (k >= 2) CK(cudaEventSynchronize(io.ev[b]));  // buffer b's previous copy is done
+    const off_t off = (off_t)sizeof(KlrmHeader) + (off_t)(M->row0 + r) * rowb;
+    char* hb = static_cast<char*>(io.host[b]);
+    if (!io_parallel((size_t)nr * rowb, [&](size_t lo, size_t len) {
+          return pread_all(fd, hb + lo, len, off + (off_t)lo);
+        }))
+      return set_err(KSVD_ECONFIG, "KLRM: short read at row %lld", (long long)(M->row0 + r));
+    if (M->dtype == KSVD_F64) {
+      CK(cudaMemcpy2DAsync((char*)M->A + (size_t)r * M->lda * es, (size_t)M->lda * es,
+                           io.host[b], (size_t)rowb, (size_t)rowb, (size_t)nr,
+                           cudaMemcpyHostToDevice, s));
+    } else {
+      CK(cudaMemcpyAsync(io.dev, io.host[b], (size_t)nr * rowb, cudaMemcpyHostToDevice, s));
+      TRY(launch(c, KC_OTHER, k_f64_to_f32_rows, dim3((unsigned)std::min<int64_t>(
+                                                            cdiv(nr * n, kThreads), 65535)),
+                 dim3(kThreads), 0, (const double*)io.dev, nr, n,
+                 (float*)M->A + (size_t)r * M->lda, M->lda));
+    }
+    CK(cudaEventRecord(io.ev[b], s));
+  }
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+static int klrm_write_from(ksvd_mat* M, int fd) {
+  ksvd_ctx* c = M->ctx;
+  cudaStream_t s = c->stream;
+  const int64_t n = M->n, mloc = M->mloc;
+  if (mloc == 0) return 0;
+  const int64_t rowb = n * 8;
+  const int64_t rpc = std::max<int64_t>(1, io_chunk_bytes() / rowb);
+  const size_t cbytes = (size_t)rpc * rowb;
+  IoBuffers io;
+  CK(cudaHostAlloc(&io.host[0], cbytes, cudaHostAllocDefault));
+  if (M->dtype == KSVD_F32) CK(cudaMalloc((void**)&io.dev, cbytes));
+  const size_t es = esize(M->dtype);
+  for (int64_t r = 0; r < mloc; r += rpc) {
+    const int64_t nr = std::min(rpc, mloc - r);
+    if (M->dtype == KSVD_F64) {
+      CK(cudaMemcpy2DAsync(io.host[0], (size_t)rowb, (char*)M->A + (size_t)r * M->lda * es,
+                           (size_t)M->lda * es, (size_t)rowb, (size_t)nr,
+                           cudaMemcpyDeviceToHost, s));
+    } else {
+      TRY(launch(c, KC_OTHER, k_f32_to_f64_rows, dim3((unsigned)std::min<int64_t>(
+                                                            cdiv(nr * n, kThreads), 65535)),
+                 dim3(kThreads), 0, (const float*)M->A + (size_t)r * M->lda, M->lda, nr, n,
+                 io.dev));
+      CK(cudaMemcpyAsync(io.host[0], io.dev, (size_t)nr * rowb, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    const off_t off = (off_t)sizeof(KlrmHeader) + (off_t)(M->row0 + r) * rowb;
+    const char* hb = static_cast<const char*>(io.host[0]);
+    if (!io_parallel((size_t)nr * rowb, [&](size_t lo, size_t len) {
+          return pwrite_all(fd, hb + lo, len, off + (off_t)lo);
+        }))
+      return set_err(KSVD_ERUNTIME, "KLRM: write failed at row %lld", (long long)(M->row0 + r));
+  }
+  return 0;
+}
+
 // ---------------------------------------------------------------------------
 // C ABI
 extern "C" {
@@ -1192,7 +1356,14 @@ static int matrix_new(ksvd_ctx* c, const void* rows, int64_t m, int64_t n, int64
     free_matrix(M);
     return rc;
   }
-  if (mloc > 0) {
+  if (mloc > 0 && rows == nullptr && M->lda > n) {  // streamed in later: zero the padding
+    cudaError_t e = cudaMemsetAsync(M->A, 0, (size_t)mloc * M->lda * es, c->stream);
+    if (e != cudaSuccess) {
+      free_matrix(M);
+      return set_err(KSVD_ERUNTIME, "memset: %s", cudaGetErrorString(e));
+    }
+  }
+  if (mloc > 0 && rows != nullptr) {
     if (M->lda > n) {
       cudaError_t e = cudaMemsetAsync(M->A, 0, (size_t)mloc * M->lda * es, c->stream);
       if (e != cudaSuccess) {
@@ -1217,12 +1388,14 @@ static int matrix_new(ksvd_ctx* c, const void* rows, int64_t m, int64_t n, int64
 
 int ksvd_matrix_from_host(ksvd_ctx* c, const void* rows, int64_t m, int64_t n, int64_t row0,
                           int64_t mloc, int64_t src_ld, int dtype, ksvd_mat** out) {
+  if (mloc > 0 && !rows) return set_err(KSVD_ECONFIG, "null row pointer");
   return matrix_new(c, rows, m, n, row0, mloc, src_ld, dtype, cudaMemcpyHostToDevice, out);
 }
 
 int ksvd_matrix_from_device(ksvd_ctx* c, const void* rows, int64_t m, int64_t n,
                             int64_t row0, int64_t mloc, int64_t src_ld, int dtype,
                             ksvd_mat** out) {
+  if (mloc > 0 && !rows) return set_err(KSVD_ECONFIG, "null row pointer");
   return matrix_new(c, rows, m, n, row0, mloc, src_ld, dtype, cudaMemcpyDeviceToDevice, out);
 }
 
@@ -1271,6 +1444,64 @@ int ksvd_matrix_gen_factors(ksvd_mat* M, double* Ps_local, double* Q, int* r) {
                        c->stream));
   CK(cudaStreamSynchronize(c->stream));
   return 0;
+}
+
+int ksvd_matrix_from_klrm(ksvd_ctx* c, const char* path, int dtype, ksvd_mat** out) {
+  if (dtype != KSVD_F64 && dtype != KSVD_F32) return set_err(KSVD_ECONFIG, "dtype %d", dtype);
+  const int fd = open(path, O_RDONLY);
+  if (fd < 0) return set_err(KSVD_ECONFIG, "%s: cannot open", path);
+  struct FdGuard {
+    int fd;
+    ~FdGuard() { close(fd); }
+  } guard{fd};
+  KlrmHeader h{};
+  if (!pread_all(fd, &h, sizeof h, 0)) return set_err(KSVD_ECONFIG, "%s: truncated header", path);
+  if (memcmp(h.magic, "KLRM", 4) != 0)
+    return set_err(KSVD_ECONFIG, "%s: bad magic %.4s, expected KLRM", path, h.magic);
+  if (h.version != 1)
+    return set_err(KSVD_ECONFIG, "%s: unsupported format version %u", path, h.version);
+  const off_t size = lseek(fd, 0, SEEK_END);
+  const unsigned long long want = (unsigned long long)h.rows * h.cols * 8ull;
+  const unsigned long long have =
+      size > (off_t)sizeof h ? (unsigned long long)(size - (off_t)sizeof h) : 0ull;
+  if (have < want)
+    return set_err(KSVD_ECONFIG, "%s: payload holds %llu bytes, header promises %llu", path,
+                   have, want);
+  const int64_t m = (int64_t)h.rows, n = (int64_t)h.cols;
+  const int64_t base = m / c->nranks, extra = m % c->nranks;
+  const int64_t row0 = c->rank * base + std::min<int64_t>(c->rank, extra);
+  const int64_t mloc = base + (c->rank < extra ? 1 : 0);
+  ksvd_mat* M = nullptr;
+  TRY(matrix_new(c, nullptr, m, n, row0, mloc, n, dtype, cudaMemcpyHostToDevice, &M));
+  const int rc = klrm_read_into(M, fd);
+  if (rc) {
+    free_matrix(M);
+    return rc;
+  }
+  *out = M;
+  return 0;
+}
+
+int ksvd_matrix_to_klrm(ksvd_mat* M, const char* path) {
+  ksvd_ctx* c = M->ctx;
+  CK(cudaSetDevice(c->device));
+  const int fd = open(path, O_WRONLY | O_CREAT, 0644);
+  if (fd < 0) return set_err(KSVD_ERUNTIME, "%s: cannot open for writing", path);
+  struct FdGuard {
+    int fd;
+    ~FdGuard() { close(fd); }
+  } guard{fd};
+  if (c->rank == 0) {
+    KlrmHeader h{};
+    memcpy(h.magic, "KLRM", 4);
+    h.version = 1;
+    h.rows = (uint64_t)M->m;
+    h.cols = (uint64_t)M->n;
+    const off_t total = (off_t)sizeof h + (off_t)M->m * M->n * 8;
+    if (ftruncate(fd, total) != 0 || !pwrite_all(fd, &h, sizeof h, 0))
+      return set_err(KSVD_ERUNTIME, "%s: cannot write the header", path);
+  }
+  return klrm_write_from(M, fd);
 }
 
 int ksvd_matrix_free(ksvd_mat* M) { return free_matrix(M); }

@@ -76,7 +76,7 @@ def _free_matrix(handle):
 
 class DeviceMatrix(LinearOperator):
     """Dense m x n matrix (this rank's row shard) in HBM, row-major, leading
-    dimension padded to 512 bytes."""
+    dimension padded to 16 bytes (one TMA / vector-load granule)."""
 
     def __init__(self, handle, ctx: _lib.Context, shape, row0: int, m_local: int,
                  dtype: np.dtype):
