@@ -29,6 +29,7 @@ from .errors import ConfigError, NumericalError, ShapeMismatchError  # noqa: F40
 
 # Stream tag of the GK start vector (reference linops.py:46).
 GK_START = 4
+BENCH_MATRIX, BENCH_METHOD = 12, 13  # reference linops.py:54-55 stream tags
 
 
 def substream(seed: int, *path: int) -> np.random.Generator:
@@ -38,6 +39,13 @@ def substream(seed: int, *path: int) -> np.random.Generator:
         raise ConfigError("seed must be a non-negative int, got None")
     seq = np.random.SeedSequence(entropy=int(seed), spawn_key=tuple(int(p) for p in path))
     return np.random.Generator(np.random.Philox(seq))
+
+
+def derive_seed(seed: int, *path: int) -> int:
+    """Child seed for a component that takes its own seed (reference
+    linops.py:72-76): first u64 word of SeedSequence(seed, spawn_key=path)."""
+    seq = np.random.SeedSequence(entropy=int(seed), spawn_key=tuple(int(p) for p in path))
+    return int(seq.generate_state(1, dtype=np.uint64)[0])
 
 
 def row_partition(m: int, nranks: int, rank: int) -> tuple[int, int]:
