@@ -49,6 +49,20 @@ struct HostProg {
   int pad;
 };
 
+// Programmatic dependent launch (ksvd.cu launch_step): wait for the
+// preceding grid's completion + memory flush / let the next grid launch.
+// Every CTA of a kernel launched with the attribute calls pdl_wait() before
+// reading its predecessor's outputs and before exiting.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// g_pdl_trig bit 0: gemv kernels trigger early, bit 1: CGS kernels do
+// (otherwise the trigger is implicit at CTA exit); KSVD_PDL_TRIG overrides.
+// Measured: 1 is best -- an early CGS trigger parks the next gemv's CTAs
+// beside the cooperative grid and costs ~5% on config 2.
+__device__ int g_pdl_trig = 1;
+__device__ __forceinline__ void pdl_trigger(int bit) {
+  if (g_pdl_trig & bit) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ bool halted(const DevState* st) {
   return *reinterpret_cast<const volatile int*>(&st->status) != ST_RUNNING;
 }
@@ -174,6 +188,8 @@ k_gemv_n2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nc
           const double* __restrict__ p_scale, double* __restrict__ p_dst, int64_t n_true,
           double* __restrict__ part, const DevState* st) {
   static_assert(RB % 8 == 0, "rows per iteration: multiple of 8");
+  pdl_wait();
+  pdl_trigger(1);
   if (halted(st)) return;
   constexpr int V = AVec<TA>::V;
   constexpr int CW = 32 * U;
@@ -437,6 +453,8 @@ k_gemv_t(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
          int64_t rows_per_split, const double* __restrict__ q_src,
          const double* __restrict__ q_scale, double* __restrict__ q_dst,
          double* __restrict__ part, int64_t ldz, const DevState* st) {
+  pdl_wait();
+  pdl_trigger(1);
   if (halted(st)) return;
   constexpr int V = AVec<TA>::V;
   constexpr int TPG = kThreads / RG;
@@ -517,6 +535,8 @@ k_gemv_t2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
           int64_t /*unused*/, const double* __restrict__ q_src,
           const double* __restrict__ q_scale, double* __restrict__ q_dst,
           double* __restrict__ part, int64_t ldz, const DevState* st) {
+  pdl_wait();
+  pdl_trigger(1);
   if (halted(st)) return;
   constexpr int V = AVec<TA>::V;
   constexpr int TPG = kThreads / RG;
@@ -884,6 +904,8 @@ __device__ __forceinline__ void coop_reduce_cols(const double* part, int ncols, 
 template <int RPL>
 __global__ void __launch_bounds__(kThreads)
 k_cgs2_coop(CgsCoopArgs a) {
+  pdl_wait();
+  pdl_trigger(2);
   if (halted(a.st)) return;
   constexpr int CH = 32 * RPL;  // rows per chunk
   extern __shared__ double colacc[];  // ncols (dot accumulators)
@@ -1042,7 +1064,6 @@ k_cgs2_tile(CgsCoopArgs a) {
   unsigned long long t_entry = 0;
   if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0)
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_entry));
-  if (halted(a.st)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double tred[kWarps][32 * MAXE];
   __shared__ __align__(8) unsigned long long mbar;
@@ -1081,6 +1102,17 @@ k_cgs2_tile(CgsCoopArgs a) {
             "l"(src), "r"(bytes), "r"(bar)
             : "memory");
       }
+  }
+  // The basis columns were written >= 2 launches back (complete once the
+  // predecessor passed its own pdl_wait), so the tile copy above may run
+  // ahead of this wait; the partial sums / x below may not.
+  pdl_wait();
+  pdl_trigger(2);
+  if (halted(a.st)) {  // drain the copy into this CTA's smem before exiting
+    if (threadIdx.x == 0)
+      while (!mbar_try_wait(bar, 0)) {
+      }
+    return;
   }
   // [0] finalisation of the split partial sums of A^T q (overlaps the copy)
   if (a.fpart) {

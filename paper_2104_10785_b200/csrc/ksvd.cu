@@ -122,16 +122,43 @@ static int collect_profile(ksvd_ctx* c) {
   return 0;
 }
 
-template <typename Kern, typename... Args>
-static int launch(ksvd_ctx* c, int cls, Kern kernel, dim3 grid, dim3 block,
-                  size_t smem, Args... args) {
+// Programmatic dependent launch for the GK step kernels (single rank): the
+// next kernel's CTAs are scheduled while the current one drains and run
+// their prologue (k_cgs2_tile: the TMA load of the basis tile) before
+// griddepcontrol.wait.  Every kernel launched this way calls pdl_wait() in
+// every CTA before touching its predecessor's outputs (kernels.cuh).
+static bool pdl_enabled(const ksvd_ctx* c) {
+  static const bool off = [] {
+    const char* e = getenv("KSVD_PDL");
+    return e && strcmp(e, "0") == 0;
+  }();
+  return !off && c->comm == nullptr;
+}
+
+template <typename... KArgs, typename... Args>
+static int launch_impl(ksvd_ctx* c, int cls, bool pdl, void (*kernel)(KArgs...), dim3 grid,
+                       dim3 block, size_t smem, Args... args) {
   cudaEvent_t a = nullptr, b = nullptr;
   if (c->profiling) {
     TRY(get_event(c, &a));
     TRY(get_event(c, &b));
     CK(cudaEventRecord(a, c->stream));
   }
-  kernel<<<grid, block, smem, c->stream>>>(args...);
+  if (pdl) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+  } else {
+    kernel<<<grid, block, smem, c->stream>>>(args...);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess)
     return set_err(KSVD_ERUNTIME, "kernel launch failed: %s", cudaGetErrorString(e));
@@ -141,6 +168,16 @@ static int launch(ksvd_ctx* c, int cls, Kern kernel, dim3 grid, dim3 block,
   }
   c->launches++;
   return 0;
+}
+template <typename... KArgs, typename... Args>
+static int launch(ksvd_ctx* c, int cls, void (*kernel)(KArgs...), dim3 grid, dim3 block,
+                  size_t smem, Args... args) {
+  return launch_impl(c, cls, false, kernel, grid, block, smem, args...);
+}
+template <typename... KArgs, typename... Args>
+static int launch_step(ksvd_ctx* c, int cls, void (*kernel)(KArgs...), dim3 grid, dim3 block,
+                       size_t smem, Args... args) {
+  return launch_impl(c, cls, pdl_enabled(c), kernel, grid, block, smem, args...);
 }
 
 static int allreduce(ksvd_ctx* c, double* buf, size_t count) {
@@ -285,11 +322,11 @@ static int enqueue_gemv_n(ksvd_mat* M, const double* p_src, const double* p_scal
   if (M->mloc == 0) return 0;
   const dim3 grid((unsigned)pn.blocks);
   if (M->dtype == KSVD_F32) {
-    TRY(launch(c, KC_GEMV_N, k_gemv_n2<float, kUnrollN32>, grid, dim3(kThreads), 0,
+    TRY(launch_step(c, KC_GEMV_N, k_gemv_n2<float, kUnrollN32>, grid, dim3(kThreads), 0,
                (const float*)M->A, M->lda, M->mloc, pn.nvec, pn.nchunks, pn.rows_per_warp,
                p_src, p_scale, p_dst, M->n, M->part_n, (const DevState*)st));
   } else {
-    TRY(launch(c, KC_GEMV_N, k_gemv_n2<double, kUnrollN64>, grid, dim3(kThreads), 0,
+    TRY(launch_step(c, KC_GEMV_N, k_gemv_n2<double, kUnrollN64>, grid, dim3(kThreads), 0,
                (const double*)M->A, M->lda, M->mloc, pn.nvec, pn.nchunks, pn.rows_per_warp,
                p_src, p_scale, p_dst, M->n, M->part_n, (const DevState*)st));
   }
@@ -311,15 +348,15 @@ static int launch_gemv_t(ksvd_mat* M, dim3 grid, const double* q_src, const doub
   const size_t abytes = (size_t)M->mloc * M->lda * esize(M->dtype);
   if (pt.rg == 8) {
     if (abytes < ((size_t)2 << 30))
-      return launch(c, KC_GEMV_T, k_gemv_t2<TA, kUnrollT, 8, 2>, grid, dim3(kThreads), 0,
+      return launch_step(c, KC_GEMV_T, k_gemv_t2<TA, kUnrollT, 8, 2>, grid, dim3(kThreads), 0,
                     (const TA*)M->A, M->lda, M->mloc, M->pn.nvec, pt.rows_per_split, q_src,
                     q_scale, q_dst, M->part_t, M->n_pad, (const DevState*)st);
-    return launch(c, KC_GEMV_T, k_gemv_t2<TA, kUnrollT, 8, 8>, grid, dim3(kThreads), 0,
+    return launch_step(c, KC_GEMV_T, k_gemv_t2<TA, kUnrollT, 8, 8>, grid, dim3(kThreads), 0,
                   (const TA*)M->A, M->lda, M->mloc, M->pn.nvec, pt.rows_per_split, q_src,
                   q_scale, q_dst, M->part_t, M->n_pad, (const DevState*)st);
   }
 #define KSVD_GT(RG)                                                                    \
-  launch(c, KC_GEMV_T, k_gemv_t<TA, kUnrollT, RG>, grid, dim3(kThreads), 0,             \
+  launch_step(c, KC_GEMV_T, k_gemv_t<TA, kUnrollT, RG>, grid, dim3(kThreads), 0,             \
          (const TA*)M->A, M->lda, M->mloc, M->pn.nvec, pt.rows_per_split, q_src, q_scale, \
          q_dst, M->part_t, M->n_pad, (const DevState*)st)
   switch (pt.rg) {
@@ -582,8 +619,21 @@ static int cgs_coop(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int n
     TRY(get_event(c, &e1));
     CK(cudaEventRecord(e0, c->stream));
   }
-  CK(cudaLaunchCooperativeKernel(kern, dim3((unsigned)G), dim3(kThreads), args, smem,
-                                 c->stream));
+  {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)G);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled(c) ? 2 : 1;
+    CK(cudaLaunchKernelExC(&cfg, kern, args));
+  }
   if (c->profiling) {
     CK(cudaEventRecord(e1, c->stream));
     c->pending.push_back({e0, e1, KC_CGS});
@@ -1226,6 +1276,10 @@ int ksvd_ctx_create(int device, int rank, int nranks, const char* uid, ksvd_ctx*
   CK(cudaGetDeviceProperties(&prop, device));
   c->sms = prop.multiProcessorCount;
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  if (const char* e = getenv("KSVD_PDL_TRIG")) {
+    const int trig = atoi(e);
+    CK(cudaMemcpyToSymbol(g_pdl_trig, &trig, sizeof trig));
+  }
   for (auto& e : c->marks) CK(cudaEventCreate(&e));
   for (auto& e : c->ring_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaHostAlloc((void**)&c->hprog, sizeof(HostProg), cudaHostAllocMapped));
