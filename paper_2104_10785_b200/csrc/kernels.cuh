@@ -866,6 +866,7 @@ struct CgsCoopArgs {
   const double* fbeta;
   const double* fp;
   unsigned long long* tdbg;  // nullable: phase timing of CTA 0
+  int redundant;  // k_cgs2_tile2: every CTA reduces all partials (else distributed + barrier)
 };
 
 // Grid-wide barrier of the cooperative launch (cooperative_groups: ~1.2 us
@@ -1254,6 +1255,274 @@ k_cgs2_tile(CgsCoopArgs a) {
     atomicAdd(a.tdbg + 7, 1ull);
   }
 }
+
+
+// Same work as k_cgs2_tile with 2 grid-wide rounds per CGS2 instead of 5:
+// every CTA reduces all G partials of every column itself (a few KB-170 KB
+// of L2 reads, cheaper than a second barrier), the partial buffers
+// ping-pong between passes, and beta^2 = ||x||^2 - ||c||^2 comes with the
+// last pass's dot products (direct-norm round only when that would cancel).
+template <int MAXE>
+__global__ void __launch_bounds__(kThreads, 1)
+k_cgs2_tile2(CgsCoopArgs a) {
+  unsigned long long t_entry = 0;
+  if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0)
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_entry));
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ double tred[kWarps][32 * MAXE];
+  __shared__ __align__(8) unsigned long long mbar;
+  __shared__ double nacc;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned G = gridDim.x;
+  const int64_t s0 = (int64_t)blockIdx.x * a.rows_per_cta;
+  const int64_t s1 = min(a.L, s0 + a.rows_per_cta);
+  const int nr = s1 > s0 ? (int)(s1 - s0) : 0;
+  const int ldt = (nr + 1) & ~1;  // 16-byte column segments
+  double* tile = reinterpret_cast<double*>(smem_raw);
+  double* cs = tile + (size_t)a.ncols * ldt;  // coefficients of the current pass
+  const uint32_t bar = smem_u32(&mbar);
+
+  // bulk-async load of the basis tile: lane 0 of warp 0 arms the mbarrier
+  // with the total byte count, then the 32 lanes of warp 0 issue the
+  // per-column copies (one thread issuing ~100+ copies serially was the
+  // largest fixed cost of this kernel); all threads wait later.
+  if (warp == 0) {
+    const uint32_t bytes = (uint32_t)ldt * 8u;
+    if (lane == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      const uint32_t total = bytes * (uint32_t)a.ncols;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                   "r"(total)
+                   : "memory");
+    }
+    __syncwarp();
+    if (bytes)
+      for (int j = lane; j < a.ncols; j += 32) {
+        const double* src = a.B + (int64_t)j * a.ldb + s0;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+            "[%3];" ::"r"(smem_u32(tile + (size_t)j * ldt)),
+            "l"(src), "r"(bytes), "r"(bar)
+            : "memory");
+      }
+  }
+  // The basis columns were written >= 2 launches back (complete once the
+  // predecessor passed its own pdl_wait), so the tile copy above may run
+  // ahead of this wait; the partial sums / x below may not.
+  pdl_wait();
+  pdl_trigger(2);
+  if (halted(a.st)) {  // drain the copy into this CTA's smem before exiting
+    if (threadIdx.x == 0)
+      while (!mbar_try_wait(bar, 0)) {
+      }
+    return;
+  }
+  // [0] finalisation of the split partial sums of A^T q (overlaps the copy)
+  if (a.fpart) {
+    for (int64_t r = s0 + threadIdx.x; r < s1; r += kThreads) {
+      double v = strided_sum(a.fpart + r, a.fld, a.fnsplit);
+      if (a.fp) v = v - (*a.fbeta) * a.fp[r];
+      a.x[r] = v;
+      flag_nonfinite(a.st, v, a.step);
+    }
+  }
+  unsigned long long tl = 0;
+  phase_mark(a.tdbg, 0, tl);
+  if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(a.tdbg + 5, tl - t_entry);
+  __syncthreads();
+  // x rows of this CTA live in registers for the whole kernel (loaded while
+  // the tile is in flight)
+  double xv[MAXE];
+#pragma unroll
+  for (int e = 0; e < MAXE; ++e) {
+    const int rl = lane + 32 * e;
+    xv[e] = rl < nr ? a.x[s0 + rl] : 0.0;
+  }
+  while (!mbar_try_wait(bar, 0)) {
+  }
+  phase_mark(a.tdbg, 1, tl);  // [1] bulk copy of the tile (+ finalisation)
+
+
+  // Ping-pong partial buffers, (ncols + 1) x G each (row ncols: norm
+  // partials): a CTA may write pass p+1's partials while slower CTAs still
+  // read pass p's, since every CTA reduces every column itself.
+  const int64_t half = (int64_t)(a.ncols + 1) * G;
+  auto partb = [&](int k) { return a.part + (k & 1) * half; };
+  double* red = cs;  // reduced sums: ncols coefficients + the norm (ncols + 1 doubles)
+
+  // xv -= tile * red[0:ncols]; the final pass stores x
+  auto update = [&](bool store) {
+    double t[MAXE];
+#pragma unroll
+    for (int e = 0; e < MAXE; ++e) t[e] = 0.0;
+#pragma unroll 4
+    for (int j = warp; j < a.ncols; j += kWarps) {
+      const double cj = red[j];
+      const double* col = tile + (size_t)j * ldt;
+#pragma unroll
+      for (int e = 0; e < MAXE; ++e) {
+        const int rl = lane + 32 * e;
+        if (rl < nr) t[e] = fma(col[rl], cj, t[e]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < MAXE; ++e) tred[warp][lane + 32 * e] = t[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < MAXE; ++e) {
+      double s = tred[0][lane + 32 * e];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) s += tred[w][lane + 32 * e];
+      xv[e] = xv[e] - s;
+      const int rl = lane + 32 * e;
+      if (store && warp == 0 && rl < nr) a.x[s0 + rl] = xv[e];
+    }
+    __syncthreads();
+  };
+  // this CTA's partial dots tile^T xv -> P[j*G + b]; optionally ||xv||^2 -> P[ncols*G + b]
+  auto dot = [&](double* P, bool with_norm) {
+    for (int q0 = 0; warp + kWarps * q0 < a.ncols; q0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = warp + kWarps * (q0 + u);
+        v[u] = 0.0;
+        if (j < a.ncols) {
+          const double* col = tile + (size_t)j * ldt;
+#pragma unroll
+          for (int e = 0; e < MAXE; ++e) {
+            const int rl = lane + 32 * e;
+            if (rl < nr) v[u] = fma(col[rl], xv[e], v[u]);
+          }
+        }
+      }
+      const double t = warp_sum8(v);
+      const int j = warp + kWarps * (q0 + warp_sum8_index(lane));
+      if ((lane & 3) == 0 && j < a.ncols) P[(int64_t)j * G + blockIdx.x] = t;
+    }
+    if (with_norm && warp == kWarps - 1) {
+      double s = 0.0;
+#pragma unroll
+      for (int e = 0; e < MAXE; ++e) s = fma(xv[e], xv[e], s);
+      s = warp_sum(s);
+      if (lane == 0) P[(int64_t)a.ncols * G + blockIdx.x] = s;
+    }
+  };
+  // red[j] = sum_b P[j*G + b] for j in [j0, j1), same fixed order in every
+  // CTA.  Redundant mode: each warp sums 4 columns with all 4 x 5 loads in
+  // flight (G <= 160); distributed mode: the grid's warps split the columns
+  // (coop_reduce_cols into a.c), one more barrier, then every CTA copies a.c.
+  auto reduce_all = [&](const double* P, int j0, int j1) {
+    if (a.redundant) {
+      for (int jb = j0 + 4 * warp; jb < j1; jb += 4 * kWarps) {
+        double sacc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const unsigned b = lane + 32 * k;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (b < G && jb + u < j1) sacc[u] += __ldcg(P + (int64_t)(jb + u) * G + b);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double t = warp_sum(sacc[u]);
+          if (lane == 0 && jb + u < j1) red[jb + u] = t;
+        }
+      }
+    } else {
+      const int gw = blockIdx.x * kWarps + warp, nw = (int)G * kWarps;
+      for (int j = j0 + gw; j < j1; j += nw) {
+        const double* p = P + (int64_t)j * G;
+        double t = 0.0;
+        for (unsigned b = lane; b < G; b += 32) t += __ldcg(p + b);
+        t = warp_sum(t);
+        if (lane == 0) a.c[j] = t;
+      }
+      grid_barrier(a.bar, G);
+      for (int j = j0 + (int)threadIdx.x; j < j1; j += kThreads) red[j] = __ldcg(a.c + j);
+    }
+    __syncthreads();
+  };
+  auto finish = [&](double nrm2) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      const double nrm = sqrt(nrm2);
+      *a.slot = nrm;
+      int stop = ST_RUNNING;
+      if (a.st->nonfinite || !isfinite(nrm)) stop = ST_NONFINITE;
+      else if (nrm < a.eps) stop = a.code;
+      if (stop != ST_RUNNING) {
+        a.st->status = stop;
+        a.st->kprime = a.step;
+        a.st->where = a.step;
+      }
+      if (a.hp && (stop != ST_RUNNING || a.side == 1)) {
+        volatile HostProg* h = a.hp;
+        if (stop != ST_RUNNING) {
+          h->status = stop;
+          h->halt_step = a.step;
+        }
+        asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(&a.hp->prog),
+                     "r"(2 * a.step + a.side)
+                     : "memory");
+      }
+    }
+  };
+
+  if (a.ncols == 0 || a.passes == 0) {
+    dot(partb(0), true);
+    grid_barrier(a.bar, G);
+    reduce_all(partb(0), a.ncols, a.ncols + 1);
+    finish(red[a.ncols]);
+  } else {
+    dot(partb(0), a.passes == 1);
+    phase_mark(a.tdbg, 2, tl);
+    for (int pass = 1; pass <= a.passes; ++pass) {
+      const bool last = pass == a.passes;
+      grid_barrier(a.bar, G);
+      phase_mark(a.tdbg, 3, tl);
+      reduce_all(partb(pass - 1), 0, a.ncols + (last ? 1 : 0));
+      phase_mark(a.tdbg, 4, tl);
+      if (!last) {
+        update(false);
+        dot(partb(pass), pass + 1 == a.passes);
+        phase_mark(a.tdbg, 2, tl);
+        continue;
+      }
+      // ||x - B c||^2 = ||x||^2 - ||c||^2 for an orthonormal B.  Exact to
+      // rounding while ||c||^2 <= 1e-6 ||x||^2 (always, after a first pass,
+      // away from breakdown); otherwise (or non-finite) take the direct norm
+      // with one more round.  The test reads identical values in every CTA.
+      double cc = 0.0;
+      for (int j = 0; j < a.ncols; ++j) cc = fma(red[j], red[j], cc);
+      const double nn = red[a.ncols];
+      const bool closed = cc <= 1e-6 * nn;
+      update(true);
+      phase_mark(a.tdbg, 2, tl);
+      if (closed) {
+        finish(nn - cc);
+      } else {
+        if (warp == kWarps - 1) {
+          double s = 0.0;
+#pragma unroll
+          for (int e = 0; e < MAXE; ++e) s = fma(xv[e], xv[e], s);
+          s = warp_sum(s);
+          if (lane == 0) partb(pass)[(int64_t)a.ncols * G + blockIdx.x] = s;
+        }
+        grid_barrier(a.bar, G);
+        reduce_all(partb(pass), a.ncols, a.ncols + 1);
+        finish(red[a.ncols]);
+      }
+    }
+  }
+  if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    atomicAdd(a.tdbg + 6, now - t_entry);
+    atomicAdd(a.tdbg + 7, 1ull);
+  }
+}
+
 
 // dst = src / val (host scalar; terminal column, bidiag.py:101)
 __global__ void __launch_bounds__(kThreads)

@@ -516,7 +516,8 @@ static bool coop_enabled(const ksvd_ctx* c, int64_t L, int ncols) {
   if (off || c->comm != nullptr || ncols > kCoopMaxCols) return false;
   const int64_t G = std::min<int64_t>(c->sms, std::max<int64_t>(1, cdiv(L, 32)));
   const int64_t rows = rup(cdiv(std::max<int64_t>(L, 1), G), 2);
-  const bool tile = rows <= 256 && sizeof(double) * (size_t)ncols * (size_t)(rows + 1) <= kTileSmemMax;
+  const bool tile =
+      rows <= 256 && sizeof(double) * (size_t)ncols * (size_t)(rows + 1) + 16 <= kTileSmemMax;
   return tile || global;
 }
 
@@ -539,9 +540,21 @@ static int tile_attr() {
   if (!done) {
     CK(cudaFuncSetAttribute(k_cgs2_tile<MAXE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kTileSmemMax));
+    CK(cudaFuncSetAttribute(k_cgs2_tile2<MAXE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kTileSmemMax));
     done = true;
   }
   return 0;
+}
+
+// k_cgs2_tile2 (2 grid rounds per CGS2) unless KSVD_CGS_SYNC=5 selects the
+// 5-round k_cgs2_tile (A/B)
+static bool tile2_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("KSVD_CGS_SYNC");
+    return !(e && strcmp(e, "5") == 0);
+  }();
+  return v;
 }
 
 static int cgs_coop(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int ncols, double* x,
@@ -580,13 +593,14 @@ static int cgs_coop(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int n
     const char* e = getenv("KSVD_TILE");
     return e && strcmp(e, "0") == 0;
   }();
-  if (!tile_off && rows <= 256 && tile_bytes <= kTileSmemMax) {
-    smem = std::max<size_t>(tile_bytes, 16);
+  const bool t2 = tile2_enabled();
+  if (!tile_off && rows <= 256 && tile_bytes + 16 <= kTileSmemMax) {
+    smem = tile_bytes + 16;  // + the (ncols + 1)-th reduced sum of k_cgs2_tile2
     switch ((int)cdiv(rows, 32)) {
-#define KSVD_TILE_CASE(E)                     \
-  case E:                                     \
-    TRY(tile_attr<E>());                      \
-    kern = (const void*)k_cgs2_tile<E>;       \
+#define KSVD_TILE_CASE(E)                                                      \
+  case E:                                                                      \
+    TRY(tile_attr<E>());                                                       \
+    kern = t2 ? (const void*)k_cgs2_tile2<E> : (const void*)k_cgs2_tile<E>;    \
     break;
       KSVD_TILE_CASE(1)
       KSVD_TILE_CASE(2)
@@ -597,7 +611,7 @@ static int cgs_coop(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int n
       KSVD_TILE_CASE(7)
       default:
         TRY(tile_attr<8>());
-        kern = (const void*)k_cgs2_tile<8>;
+        kern = t2 ? (const void*)k_cgs2_tile2<8> : (const void*)k_cgs2_tile<8>;
 #undef KSVD_TILE_CASE
     }
   } else {
@@ -609,7 +623,14 @@ static int cgs_coop(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int n
     kern = (const void*)k_cgs2_coop<kCoopRPL>;
   }
   a.rows_per_cta = (int)rows;
-  TRY(ensure_cgs(c->stream, W, G, ncols));
+  // k_cgs2_tile2 reduction mode: every CTA reads all G x (ncols + 1) partials
+  // while that is cheaper than a second grid barrier (KSVD_RED_MAX doubles)
+  static const int64_t red_max = [] {
+    const char* e = getenv("KSVD_RED_MAX");
+    return e ? (int64_t)atoll(e) : (int64_t)148 * 16;  // measured: configs 1-2
+  }();
+  a.redundant = G <= 160 && (int64_t)(ncols + 1) * G <= red_max;
+  TRY(ensure_cgs(c->stream, W, G, 2 * (ncols + 1)));  // k_cgs2_tile2: ping-pong + norm row
   a.part = W->part;
   a.c = W->c;
   a.bar = W->bar;

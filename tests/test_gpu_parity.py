@@ -278,12 +278,17 @@ print(json.dumps(out))
 
 
 @pytest.mark.parametrize("env", [{"KSVD_TILE": "0"}, {"KSVD_COOP": "0"}, {"KSVD_FORCE_NCCL": "1"},
-                                 {"KSVD_COOP_GLOBAL": "1", "KSVD_TILE": "0"}, {}])
+                                 {"KSVD_COOP_GLOBAL": "1", "KSVD_TILE": "0"},
+                                 {"KSVD_CGS_SYNC": "5"}, {"KSVD_RED_MAX": "0"},
+                                 {"KSVD_RED_MAX": "100000000"}, {"KSVD_PDL": "0"},
+                                 {"KSVD_PDL_TRIG": "3"}, {}])
 def test_cgs_paths_agree(env):
-    """The tile-resident, global-load cooperative and multi-kernel CGS2
-    paths (selected at load time) all meet the parity bar; KSVD_FORCE_NCCL
-    runs the multi-rank code path (NCCL all-reduces between the kernels)
-    over a 1-rank communicator."""
+    """The tile-resident (2-round k_cgs2_tile2 with redundant or distributed
+    reductions, 5-round k_cgs2_tile), global-load cooperative and
+    multi-kernel CGS2 paths (selected at load time) all meet the parity bar,
+    with and without programmatic dependent launch; KSVD_FORCE_NCCL runs the
+    multi-rank code path (NCCL all-reduces between the kernels) over a
+    1-rank communicator."""
     import json
     import os
     import subprocess
