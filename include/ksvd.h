@@ -174,6 +174,17 @@ int ksvd_matrix_generate(ksvd_ctx *ctx, const ksvd_gen_spec *spec, ksvd_mat **ou
  * row-major); r receives the rank.  Either pointer may be NULL. */
 int ksvd_matrix_gen_factors(ksvd_mat *mat, double *Ps_local, double *Q, int *r);
 
+/* ---- factored operator L C R^T (reference linops.py:176-205) -----------
+ * FactoredOperator(left d1 x s1, core s1 x s2, right d2 x s2): every
+ * product costs O((d1 + d2) s) and nothing of size d1 x d2 is formed.
+ * left_rows = this rank's rows [row0, row0 + mloc) of `left` (row-major, s1
+ * per row); core and right are full (row-major).  The handle is a ksvd_mat
+ * usable with every product / GK / Ritz entry point; ksvd_matrix_to_host
+ * and ksvd_matrix_to_klrm return KSVD_ECONFIG (no dense rows). */
+int ksvd_matrix_from_factors(ksvd_ctx *ctx, const double *left_rows, const double *core,
+                             const double *right, int64_t m, int64_t n, int64_t s1,
+                             int64_t s2, int64_t row0, int64_t mloc, ksvd_mat **out);
+
 /* ---- KLRM snapshots (reference matrixio.py:15-46) ------------------------
  * Little-endian header "<4sIQQ" (magic KLRM, u32 version 1, u64 rows, u64
  * cols) + rows*cols f64 row-major payload.  The reader streams this rank's

@@ -11,7 +11,7 @@ from .bidiag import (BidiagConfig, BidiagState, GKRun, bidiagonal_matrix,
                      bidiagonalize, run_gk, with_k_max)
 from .errors import ConfigError, NumericalError, ShapeMismatchError
 from .fsvd import SymTridiag, fsvd, gram_tridiag, symtridiag_eig
-from .linops import (GK_START, DeviceMatrix, LinearOperator, PartialSvd,
+from .linops import (GK_START, DeviceMatrix, FactoredOperator, LinearOperator, PartialSvd,
                      as_operator, row_partition, substream)
 from .matrixio import (read_csv_matrix, read_matrix, read_matrix_device, write_matrix,
                        write_matrix_device)
@@ -24,7 +24,7 @@ __all__ = [
     "run_gk", "with_k_max",
     "ConfigError", "NumericalError", "ShapeMismatchError",
     "SymTridiag", "fsvd", "gram_tridiag", "symtridiag_eig",
-    "GK_START", "DeviceMatrix", "LinearOperator", "PartialSvd", "as_operator",
+    "GK_START", "DeviceMatrix", "FactoredOperator", "LinearOperator", "PartialSvd", "as_operator",
     "row_partition", "substream",
     "RankReport", "count_above", "estimate_rank",
     "read_csv_matrix", "read_matrix", "read_matrix_device", "write_matrix", "write_matrix_device",

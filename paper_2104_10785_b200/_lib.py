@@ -78,6 +78,8 @@ SIGNATURES = {
     "ksvd_matrix_gen_factors": (C.c_int, [_vp, _pd, _pd, _pi]),
     "ksvd_matrix_from_klrm": (C.c_int, [_vp, C.c_char_p, C.c_int, C.POINTER(_vp)]),
     "ksvd_matrix_to_klrm": (C.c_int, [_vp, C.c_char_p]),
+    "ksvd_matrix_from_factors": (C.c_int, [_vp, _pd, _pd, _pd, C.c_int64, C.c_int64, C.c_int64,
+                                           C.c_int64, C.c_int64, C.c_int64, C.POINTER(_vp)]),
 }
 
 _lib = None

@@ -433,6 +433,24 @@ k_gemv_n_finalize(const double* __restrict__ part, int64_t part_ld, int nchunks,
   flag_nonfinite(st, s, step);
 }
 
+// y = C x (trans 0, y has s1 entries) or C^T x (trans 1, s2 entries) for
+// the s1 x s2 row-major core of a factored operator (linops.py:192-202);
+// one warp per output, fixed order.
+__global__ void __launch_bounds__(kThreads)
+k_core_gemv(const double* __restrict__ C, int64_t s1, int64_t s2, int trans,
+            const double* __restrict__ x, double* __restrict__ y, const DevState* st) {
+  if (halted(st)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int64_t outs = trans ? s2 : s1, ins = trans ? s1 : s2;
+  if (i >= outs) return;
+  double acc = 0.0;
+  for (int64_t j = lane; j < ins; j += 32)
+    acc = fma(trans ? C[j * s2 + i] : C[i * s2 + j], x[j], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) y[i] = acc;
+}
+
 // ---------------------------------------------------------------------------
 // gemv_t:  partial z = A^T q over a row split  (bidiag.py:169, linops.py:164)
 //

@@ -218,6 +218,14 @@ struct ksvd_mat {
   // generator factors (ksvd_matrix_generate): Ps = P diag(s) local rows, Q
   double *gen_ps = nullptr, *gen_q = nullptr;
   int gen_r = 0;
+  // factored operator L C R^T (ksvd_matrix_from_factors, reference
+  // linops.py:176-205): L = this rank's rows (mloc x s1), R replicated
+  // (n x s2), both dense sub-matrices; C (s1 x s2) and two vectors on device
+  struct Factored {
+    ksvd_mat *L = nullptr, *R = nullptr;
+    double *C = nullptr, *t1 = nullptr, *t2 = nullptr;
+    int64_t s1 = 0, s2 = 0;
+  }* fac = nullptr;
 };
 
 static size_t esize(int dtype) { return dtype == KSVD_F32 ? 4 : 8; }
@@ -301,6 +309,14 @@ static int free_matrix(ksvd_mat* M) {
   if (!M) return 0;
   cudaStream_t s = M->ctx->stream;
   cudaSetDevice(M->ctx->device);
+  if (M->fac) {
+    free_matrix(M->fac->L);
+    free_matrix(M->fac->R);
+    for (double* p : {M->fac->C, M->fac->t1, M->fac->t2})
+      if (p) cudaFreeAsync(p, s);
+    delete M->fac;
+    M->fac = nullptr;
+  }
   for (void* p : {(void*)M->A, (void*)M->part_n, (void*)M->part_t, (void*)M->dx, (void*)M->dy,
                   (void*)M->st0})
     if (p) cudaFreeAsync(p, s);
@@ -314,9 +330,9 @@ static int free_matrix(ksvd_mat* M) {
 // w = A p (- alpha q): partial row sums per column chunk (k_gemv_n2), then
 // the chunk sums + epilogue (k_gemv_n_finalize) unless the caller fuses the
 // finalisation into its k_cgs2_* launch (finalize = false).
-static int enqueue_gemv_n(ksvd_mat* M, const double* p_src, const double* p_scale,
-                          double* p_dst, const double* qprev, const double* alpha,
-                          double* w, DevState* st, int step, bool finalize = true) {
+static int dense_gemv_n(ksvd_mat* M, const double* p_src, const double* p_scale,
+                        double* p_dst, const double* qprev, const double* alpha,
+                        double* w, DevState* st, int step, bool finalize = true) {
   ksvd_ctx* c = M->ctx;
   const GemvNPlan& pn = M->pn;
   if (M->mloc == 0) return 0;
@@ -368,10 +384,10 @@ static int launch_gemv_t(ksvd_mat* M, dim3 grid, const double* q_src, const doub
 }
 
 // z = sum_ranks A^T q (- beta p): q_src/q_scale/q_dst per k_gemv_t.
-static int enqueue_gemv_t(ksvd_mat* M, const double* q_src, const double* q_scale,
-                          double* q_dst, const double* beta, const double* pprev,
-                          double* z, DevState* st, int step, bool check,
-                          bool finalize = true) {
+static int dense_gemv_t(ksvd_mat* M, const double* q_src, const double* q_scale,
+                        double* q_dst, const double* beta, const double* pprev,
+                        double* z, DevState* st, int step, bool check,
+                        bool finalize = true) {
   ksvd_ctx* c = M->ctx;
   const GemvTPlan& pt = M->pt;
   if (M->mloc > 0) {
@@ -398,6 +414,82 @@ static int enqueue_gemv_t(ksvd_mat* M, const double* q_src, const double* q_scal
                  dim3(kThreads), 0, z, beta, pprev, M->n, st, step));
   }
   return 0;
+}
+
+struct FinArgs {  // deferred gemv_t finalisation (phase 0 of k_cgs2_coop)
+  const double* part = nullptr;
+  int64_t ld = 0;
+  int nsplit = 0;
+  const double* beta = nullptr;
+  const double* p = nullptr;
+};
+
+// ---------------------------------------------------------------------------
+// Factored operator products (reference linops.py:192-202):
+//   A p   = L (C (R^T p))      A^T q = R (C^T (L^T q))
+// built from the dense kernels on the sub-matrices plus an s x s core
+// product; the last stage's partial sums have the k_gemv_n2 layout, so the
+// CGS kernels fuse their finalisation exactly as for a dense A.  Multi-rank:
+// L^T q is the only sharded reduction (an s-length all-reduce); R and C are
+// replicated, so z is identical on every rank without another collective.
+static int local_gemv_t(ksvd_mat* S, const double* q_src, const double* q_scale,
+                        double* q_dst, double* out, DevState* st, int step) {
+  ksvd_ctx* c = S->ctx;
+  const GemvTPlan& pt = S->pt;
+  if (S->mloc > 0) {
+    dim3 grid((unsigned)pt.ncoltiles, (unsigned)pt.nsplit);
+    TRY(launch_gemv_t<double>(S, grid, q_src, q_scale, q_dst, st));
+  } else {
+    CK(cudaMemsetAsync(S->part_t, 0, sizeof(double) * S->n_pad, c->stream));
+  }
+  return launch(c, KC_FIN, k_gemv_t_finalize, dim3((unsigned)cdiv(S->n_pad, 32)),
+                dim3(kThreads), 0, (const double*)S->part_t, S->n_pad,
+                S->mloc > 0 ? (int)pt.nsplit : 1, S->n, S->n_pad, (const double*)nullptr,
+                (const double*)nullptr, out, st, step, 0);
+}
+
+static int core_gemv(ksvd_mat* M, int trans, const double* x, double* y, DevState* st) {
+  const auto* F = M->fac;
+  const int64_t outs = trans ? F->s2 : F->s1;
+  return launch(M->ctx, KC_OTHER, k_core_gemv, dim3((unsigned)cdiv(outs, kWarps)),
+                dim3(kThreads), 0, (const double*)F->C, F->s1, F->s2, trans, x, y,
+                (const DevState*)st);
+}
+
+static int enqueue_gemv_n(ksvd_mat* M, const double* p_src, const double* p_scale,
+                          double* p_dst, const double* qprev, const double* alpha,
+                          double* w, DevState* st, int step, bool finalize = true) {
+  if (!M->fac) return dense_gemv_n(M, p_src, p_scale, p_dst, qprev, alpha, w, st, step, finalize);
+  auto* F = M->fac;
+  TRY(local_gemv_t(F->R, p_src, p_scale, p_dst, F->t1, st, step));
+  TRY(core_gemv(M, 0, F->t1, F->t2, st));
+  return dense_gemv_n(F->L, F->t2, nullptr, nullptr, qprev, alpha, w, st, step, finalize);
+}
+
+static int enqueue_gemv_t(ksvd_mat* M, const double* q_src, const double* q_scale,
+                          double* q_dst, const double* beta, const double* pprev,
+                          double* z, DevState* st, int step, bool check,
+                          bool finalize = true) {
+  if (!M->fac)
+    return dense_gemv_t(M, q_src, q_scale, q_dst, beta, pprev, z, st, step, check, finalize);
+  auto* F = M->fac;
+  TRY(local_gemv_t(F->L, q_src, q_scale, q_dst, F->t1, st, step));
+  TRY(allreduce(M->ctx, F->t1, (size_t)F->s1));
+  TRY(core_gemv(M, 1, F->t1, F->t2, st));
+  return dense_gemv_n(F->R, F->t2, nullptr, nullptr, pprev, beta, z, st, step, finalize);
+}
+
+// where the CGS kernels find the last product's partial sums
+static FinArgs fin_left(ksvd_mat* M, const double* alpha, const double* qprev) {
+  ksvd_mat* S = M->fac ? M->fac->L : M;
+  return FinArgs{S->part_n, S->mloc, S->mloc > 0 ? S->pn.nchunks : 0, alpha, qprev};
+}
+static FinArgs fin_right(ksvd_mat* M, const double* beta, const double* pprev) {
+  if (M->fac) {
+    ksvd_mat* S = M->fac->R;
+    return FinArgs{S->part_n, S->mloc, S->pn.nchunks, beta, pprev};
+  }
+  return FinArgs{M->part_t, M->n_pad, M->mloc > 0 ? (int)M->pt.nsplit : 0, beta, pprev};
 }
 
 // ---------------------------------------------------------------------------
@@ -488,13 +580,6 @@ static int cgs_impl(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int n
 constexpr int kCoopRPL = 4;
 constexpr int kCoopMaxCols = 12288;  // colacc in dynamic shared memory (96 KB)
 
-struct FinArgs {  // deferred gemv_t finalisation (phase 0 of k_cgs2_coop)
-  const double* part = nullptr;
-  int64_t ld = 0;
-  int nsplit = 0;
-  const double* beta = nullptr;
-  const double* p = nullptr;
-};
 
 constexpr size_t kTileSmemMax = 200 * 1024;  // basis tile budget of k_cgs2_tile
 
@@ -775,8 +860,7 @@ static int enqueue_step(ksvd_run* R, int i) {
   SecTimer t_cgs(2);
   // CGS2 against Q[:, :i]; beta_{i+1} = ||w||; beta < eps -> breakdown
   if (coop_enabled(c, M->mloc, i)) {
-    FinArgs fin{M->part_n, M->mloc, M->mloc > 0 ? M->pn.nchunks : 0, R->alpha + i,
-                Qcol(R, i - 1)};
+    const FinArgs fin = fin_left(M, R->alpha + i, Qcol(R, i - 1));
     TRY(cgs_coop(c, &R->left, R->Q, R->ldq, i, R->w, M->mloc, R->reorth, R->eps,
                  R->beta + i + 1, R->st, i, ST_BETA_BREAK, R->M->ctx->dprog, 0, fin));
   } else {
@@ -795,8 +879,7 @@ static int enqueue_step(ksvd_run* R, int i) {
   if (coop_enabled(c, M->n, i)) {
     TRY(enqueue_gemv_t(M, R->w, R->beta + i + 1, Qcol(R, i), R->beta + i + 1, Pcol(R, i - 1),
                        R->z, R->st, i, true, /*finalize=*/false));
-    FinArgs fin{M->part_t, M->n_pad, M->mloc > 0 ? (int)M->pt.nsplit : 0, R->beta + i + 1,
-                Pcol(R, i - 1)};
+    const FinArgs fin = fin_right(M, R->beta + i + 1, Pcol(R, i - 1));
     TRY(cgs_coop(c, &R->right, R->P, R->ldp, i, R->z, M->n, R->reorth, R->eps,
                  R->alpha + i + 1, R->st, i, ST_ALPHA_BREAK, R->M->ctx->dprog, 1, fin));
   } else {
@@ -855,7 +938,7 @@ static int set_l2_window(ksvd_mat* M, bool on) {
   int max_persist = 0, max_window = 0;
   CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device));
   CK(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, c->device));
-  const size_t abytes = (size_t)M->mloc * M->lda * esize(M->dtype);
+  const size_t abytes = M->A ? (size_t)M->mloc * M->lda * esize(M->dtype) : 0;
   if (max_persist <= 0 || max_window <= 0 || abytes == 0) return 0;
   cudaStreamAttrValue v{};
   if (on) {
@@ -968,6 +1051,19 @@ static int enqueue_multi_rhs(ksvd_mat* M, const double* X, int64_t ldx, int k,
 
 static int multi_rhs(ksvd_mat* M, const double* X, int64_t ldx, int k, const double* sigma,
                      double* Y, int64_t ldy) {
+  if (M->fac) {  // small and latency-bound: one factored product per column
+    CK(cudaMemsetAsync(M->st0, 0, sizeof(DevState), M->ctx->stream));
+    for (int j = 0; j < k; ++j) {
+      double* y = Y + (int64_t)j * ldy;
+      TRY(enqueue_gemv_n(M, X + (int64_t)j * ldx, nullptr, nullptr, nullptr, nullptr, y,
+                         M->st0, 0));
+      if (sigma && M->mloc > 0)
+        TRY(launch(M->ctx, KC_OTHER, k_scale, dim3((unsigned)cdiv(M->mloc, kThreads)),
+                   dim3(kThreads), 0, (const double*)y, sigma + j, y, M->mloc,
+                   (const DevState*)M->st0));
+    }
+    return 0;
+  }
   if (M->dtype == KSVD_F32) return enqueue_multi_rhs<float>(M, X, ldx, k, sigma, Y, ldy);
   return enqueue_multi_rhs<double>(M, X, ldx, k, sigma, Y, ldy);
 }
@@ -1558,6 +1654,7 @@ int ksvd_matrix_from_klrm(ksvd_ctx* c, const char* path, int dtype, ksvd_mat** o
 }
 
 int ksvd_matrix_to_klrm(ksvd_mat* M, const char* path) {
+  if (M->fac) return set_err(KSVD_ECONFIG, "factored operator has no dense rows");
   ksvd_ctx* c = M->ctx;
   CK(cudaSetDevice(c->device));
   const int fd = open(path, O_WRONLY | O_CREAT, 0644);
@@ -1579,6 +1676,67 @@ int ksvd_matrix_to_klrm(ksvd_mat* M, const char* path) {
   return klrm_write_from(M, fd);
 }
 
+int ksvd_matrix_from_factors(ksvd_ctx* c, const double* left_rows, const double* core,
+                             const double* right, int64_t m, int64_t n, int64_t s1, int64_t s2,
+                             int64_t row0, int64_t mloc, ksvd_mat** out) {
+  if (m < 1 || n < 1 || s1 < 1 || s2 < 1)
+    return set_err(KSVD_ECONFIG, "factored operator: %lldx%lld with core %lldx%lld",
+                   (long long)m, (long long)n, (long long)s1, (long long)s2);
+  if (row0 < 0 || mloc < 0 || row0 + mloc > m)
+    return set_err(KSVD_ECONFIG, "row shard [%lld, %lld) outside %lld rows", (long long)row0,
+                   (long long)(row0 + mloc), (long long)m);
+  if ((mloc > 0 && !left_rows) || !core || !right)
+    return set_err(KSVD_ECONFIG, "null factor pointer");
+  CK(cudaSetDevice(c->device));
+  auto* M = new ksvd_mat();
+  M->ctx = c;
+  M->m = m;
+  M->n = n;
+  M->row0 = row0;
+  M->mloc = mloc;
+  M->dtype = KSVD_F64;
+  M->n_pad = rup(n, 64);
+  M->m_pad = rup(std::max<int64_t>(mloc, 1), 64);
+  M->fac = new ksvd_mat::Factored();
+  M->fac->s1 = s1;
+  M->fac->s2 = s2;
+  auto fail = [&](int rc) {
+    free_matrix(M);
+    return rc;
+  };
+  int rc = matrix_new(c, left_rows, std::max<int64_t>(mloc, 1), s1, 0, mloc, s1, KSVD_F64,
+                      cudaMemcpyHostToDevice, &M->fac->L);
+  if (!rc)
+    rc = matrix_new(c, right, n, s2, 0, n, s2, KSVD_F64, cudaMemcpyHostToDevice, &M->fac->R);
+  if (rc) return fail(rc);
+  cudaStream_t st = c->stream;
+  const size_t vec = sizeof(double) * std::max(M->n_pad, M->m_pad);
+  const size_t sv = sizeof(double) * rup(std::max(s1, s2), 64);
+  cudaError_t e = cudaSuccess;
+  auto ok = [&](cudaError_t x) {
+    if (e == cudaSuccess) e = x;
+  };
+  ok(cudaMallocAsync((void**)&M->fac->C, sizeof(double) * s1 * s2, st));
+  ok(cudaMallocAsync((void**)&M->fac->t1, sv, st));
+  ok(cudaMallocAsync((void**)&M->fac->t2, sv, st));
+  ok(cudaMallocAsync((void**)&M->dx, vec, st));
+  ok(cudaMallocAsync((void**)&M->dy, vec, st));
+  ok(cudaMallocAsync((void**)&M->st0, sizeof(DevState), st));
+  if (e == cudaSuccess) {
+    ok(cudaMemcpyAsync(M->fac->C, core, sizeof(double) * s1 * s2, cudaMemcpyHostToDevice, st));
+    ok(cudaMemsetAsync(M->fac->t1, 0, sv, st));
+    ok(cudaMemsetAsync(M->fac->t2, 0, sv, st));
+    ok(cudaMemsetAsync(M->dx, 0, vec, st));
+    ok(cudaMemsetAsync(M->dy, 0, vec, st));
+    ok(cudaMemsetAsync(M->st0, 0, sizeof(DevState), st));
+    ok(cudaStreamSynchronize(st));
+  }
+  if (e != cudaSuccess)
+    return fail(set_err(KSVD_ERUNTIME, "factored operator: %s", cudaGetErrorString(e)));
+  *out = M;
+  return 0;
+}
+
 int ksvd_matrix_free(ksvd_mat* M) { return free_matrix(M); }
 
 int ksvd_matrix_shape(ksvd_mat* M, int64_t* m, int64_t* n, int64_t* row0, int64_t* mloc,
@@ -1593,6 +1751,7 @@ int ksvd_matrix_shape(ksvd_mat* M, int64_t* m, int64_t* n, int64_t* row0, int64_
 }
 
 int ksvd_matrix_to_host(ksvd_mat* M, void* rows) {
+  if (M->fac) return set_err(KSVD_ECONFIG, "factored operator has no dense rows");
   ksvd_ctx* c = M->ctx;
   CK(cudaSetDevice(c->device));
   if (M->mloc == 0) return 0;

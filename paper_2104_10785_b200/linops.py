@@ -218,6 +218,49 @@ class DeviceMatrix(LinearOperator):
         self._fin()
 
 
+class FactoredOperator(DeviceMatrix):
+    """left @ core @ right^T applied without forming the product (reference
+    linops.py:176-205), resident on the device.
+
+    left is d1 x s1, core s1 x s2, right d2 x s2; products cost
+    O((d1 + d2) s) per vector (ksvd_matrix_from_factors: the dense gemv
+    kernels on the factors plus an s1 x s2 core product), so fsvd /
+    estimate_rank / bidiagonalize run on it exactly as on a DeviceMatrix --
+    the retraction caller's (manifold.py:121-130, 180) large targets never
+    materialize d1 x d2.  Under a multi-rank context this rank holds its row
+    shard of `left`; core and right are replicated."""
+
+    def __init__(self, left, core, right, ctx: _lib.Context | None = None):
+        left, core, right = (self._check(x) for x in (left, core, right))
+        if left.shape[1] != core.shape[0] or right.shape[1] != core.shape[1]:
+            raise ShapeMismatchError(
+                f"factored operator: left {left.shape}, core {core.shape}, "
+                f"right {right.shape} do not chain")
+        ctx = ctx or _lib.get_context()
+        m, n = left.shape[0], right.shape[0]
+        r0, ml = row_partition(m, ctx.nranks, ctx.rank)
+        rows = np.ascontiguousarray(left[r0:r0 + ml])
+        core_c, right_c = np.ascontiguousarray(core), np.ascontiguousarray(right)
+        h = C.c_void_p()
+        _lib.check(_lib.load_library().ksvd_matrix_from_factors(
+            ctx.handle, _lib.dptr(rows) if ml else None, _lib.dptr(core_c), _lib.dptr(right_c),
+            m, n, core.shape[0], core.shape[1], r0, ml, C.byref(h)))
+        super().__init__(h, ctx, (m, n), r0, ml, np.float64)
+        self.left, self.core, self.right = left, core, right
+
+    @staticmethod
+    def _check(X) -> np.ndarray:
+        X = np.asarray(X, dtype=np.float64)
+        if X.ndim != 2:
+            raise ShapeMismatchError(f"expected a 2-d matrix, got shape {X.shape}")
+        return X
+
+    def to_dense(self):
+        """This rank's rows of left @ core @ right^T, formed on the device
+        (one factored product per column)."""
+        return self.matmat(np.eye(self.shape[1]))
+
+
 def shape_of(A) -> tuple[int, int]:
     """(m, n) without touching the device (validation before upload)."""
     if isinstance(A, DeviceMatrix):
@@ -235,6 +278,10 @@ def as_operator(A) -> DeviceMatrix:
     Python-level operators cannot run on this path and are rejected."""
     if isinstance(A, DeviceMatrix):
         return A
+    if all(hasattr(A, f) for f in ("left", "core", "right")) and hasattr(A, "matvec"):
+        # the reference's FactoredOperator (linops.py:176-205): same factors
+        # on the device, never formed
+        return FactoredOperator(A.left, A.core, A.right)
     if isinstance(A, LinearOperator) or (hasattr(A, "matvec") and hasattr(A, "rmatvec")
                                          and not isinstance(A, np.ndarray)):
         raise ConfigError(

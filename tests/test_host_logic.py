@@ -119,3 +119,13 @@ def test_substream_matches_reference_contract():
     assert not np.array_equal(a, substream(4, 2).standard_normal(8))
     with pytest.raises(ConfigError):
         substream(None, 1)
+
+
+def test_factored_operator_shape_errors_before_device_work():
+    import paper_2104_10785_b200 as K
+    with pytest.raises(K.ShapeMismatchError):
+        K.FactoredOperator(np.ones((5, 3)), np.ones((2, 2)), np.ones((4, 2)))
+    with pytest.raises(K.ShapeMismatchError):
+        K.FactoredOperator(np.ones((5, 2)), np.ones((2, 3)), np.ones((4, 2)))
+    with pytest.raises(K.ShapeMismatchError):
+        K.FactoredOperator(np.ones(5), np.ones((1, 1)), np.ones((4, 1)))
