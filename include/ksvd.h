@@ -146,6 +146,22 @@ int ksvd_run_bases(ksvd_run *run, double *Q, int q_cols, double *P,
  * V: n x take (column-major); n_good receives the kept column count. */
 int ksvd_ritz(ksvd_run *run, const double *G, const double *sigma, int take,
               int orthonormalize_u, double *U, double *V, int *n_good);
+/* ---- restarted mode (beyond reference semantics) ---
+ * Thick restart of a finished, non-broken-down run of k = k' steps, in the
+ * transposed ("A^T Q = P T") form where T is the k x k upper bidiagonal of
+ * alphas (diagonal) and betas (superdiagonal): with T = Uh diag(s) Vh^T,
+ * keep l Ritz pairs -- Q[:, :l] = Q[:, :k] X, Q[:, l] = q_{k+1},
+ * P[:, :l] = P[:, :k] Y (X = Vh[:, :l], Y = Uh[:, :l], both k x l
+ * column-major) -- then z = A^T q_{l+1}, CGS2 against P[:, :l] (the
+ * coefficients are the restart spike rho_i = beta_{k+1} Uh[k-1, i]),
+ * alpha_{l+1} = ||z||, and resume the standard loop at step l+1 up to
+ * k_new.  ksvd_run_info then reports the new alphas[l..k'-1] and
+ * betas[l+1..k'] (entries below are zero). */
+int ksvd_run_restart(ksvd_run *run, int l, const double *X, const double *Y, int k_new);
+/* U = Q[:, :kq] X (m_local x take), V = P[:, :kp] Y (n x take), sign fix
+ * (linops.py:271-282 rule on V).  X: kq x take, Y: kp x take col-major. */
+int ksvd_run_ritz_bases(ksvd_run *run, const double *X, int kq, const double *Y, int kp,
+                        int take, double *U, double *V);
 int ksvd_run_free(ksvd_run *run);
 
 /* ---- synthetic matrices (BASELINE.json configs 3-5) -----------------------
@@ -208,6 +224,12 @@ int ksvd_symtridiag_eig(int n, const double *d, const double *e, int vectors,
  * high relative accuracy (bisection on the Golub-Kahan tridiagonal); the
  * rank estimator's "tiny bidiagonal SVD" (rank.py:64). */
 int ksvd_bidiag_sv2(int k, const double *alphas, const double *betas, double *theta);
+/* Dense SVD T = U diag(s) V^T of a small k x k matrix (column-major; s
+ * descending): the projected matrix of the restarted mode, whose first
+ * rows carry the restart spike and so is not bidiagonal (one-sided Jacobi,
+ * high relative accuracy).  No reference counterpart: SURVEY.md 8(f) row 3
+ * (Ritz-vector restarts are a non-goal of the reference). */
+int ksvd_dense_svd(int k, const double *T, double *U, double *s, double *V);
 
 #ifdef __cplusplus
 }

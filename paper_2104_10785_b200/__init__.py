@@ -16,6 +16,7 @@ from .linops import (GK_START, DeviceMatrix, FactoredOperator, LinearOperator, P
 from .matrixio import (read_csv_matrix, read_matrix, read_matrix_device, write_matrix,
                        write_matrix_device)
 from .rank import RankReport, count_above, estimate_rank
+from .restart import RestartInfo, fsvd_restarted
 
 __version__ = "0.1.0"
 
@@ -26,7 +27,7 @@ __all__ = [
     "SymTridiag", "fsvd", "gram_tridiag", "symtridiag_eig",
     "GK_START", "DeviceMatrix", "FactoredOperator", "LinearOperator", "PartialSvd", "as_operator",
     "row_partition", "substream",
-    "RankReport", "count_above", "estimate_rank",
+    "RankReport", "count_above", "estimate_rank", "RestartInfo", "fsvd_restarted",
     "read_csv_matrix", "read_matrix", "read_matrix_device", "write_matrix", "write_matrix_device",
     "__version__",
 ]

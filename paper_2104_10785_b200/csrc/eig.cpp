@@ -211,3 +211,85 @@ extern "C" int ksvd_bidiag_sv2(int k, const double* alphas, const double* betas,
   for (int j = 0; j < k; ++j) theta[j] = th[j];
   return KSVD_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Dense SVD of the small k x k projected matrix of the restarted mode
+// (T = [diag(sigma) rho; 0 bidiagonal], paper_2104_10785_b200/restart.py):
+// one-sided Jacobi (Hestenes) on the columns of W = T, V accumulating the
+// rotations; converged when every column pair is orthogonal to k * eps
+// relative (the rounding level of the pair's dot product), which gives every
+// singular value to high relative accuracy.
+// T, U, V column-major k x k; s descending; sign of each column pair fixed so
+// that U[:, j] = T V[:, j] / s_j (U columns of zero singular values are left
+// as the normalised zero column, i.e. 0).
+extern "C" int ksvd_dense_svd(int k, const double* T, double* U, double* s, double* V) {
+  if (k <= 0) return ksvd_set_error_from_host(KSVD_ECONFIG, "empty matrix");
+  const size_t K = (size_t)k;
+  std::vector<double> W(T, T + K * K), Vm(K * K, 0.0);
+  for (size_t i = 0; i < K; ++i) Vm[i * K + i] = 1.0;
+  auto col = [&](std::vector<double>& X, int j) { return X.data() + (size_t)j * K; };
+  const double tol = std::max(1e-15, (double)K * DBL_EPSILON);
+  // columns below eps ||T||_F are numerically zero: rotating them against
+  // the others only stirs rounding noise (exactly rank-deficient T -- a
+  // breakdown -- would never pass the relative test)
+  double fro2 = 0.0;
+  for (size_t i = 0; i < K * K; ++i) fro2 += W[i] * W[i];
+  const double zero2 = fro2 * DBL_EPSILON * DBL_EPSILON;
+  bool done = false;
+  double worst = 0.0;
+  for (int sweep = 0; sweep < 80 && !done; ++sweep) {
+    done = true;
+    worst = 0.0;
+    for (int p = 0; p < k - 1; ++p) {
+      for (int q = p + 1; q < k; ++q) {
+        double* wp = col(W, p);
+        double* wq = col(W, q);
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (size_t i = 0; i < K; ++i) {
+          a += wp[i] * wp[i];
+          b += wq[i] * wq[i];
+          g += wp[i] * wq[i];
+        }
+        if (g == 0.0 || a <= zero2 || b <= zero2 || std::fabs(g) <= tol * std::sqrt(a * b))
+          continue;
+        worst = std::max(worst, std::fabs(g) / std::sqrt(a * b));
+        done = false;
+        const double zeta = (b - a) / (2.0 * g);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
+        double* vp = col(Vm, p);
+        double* vq = col(Vm, q);
+        for (size_t i = 0; i < K; ++i) {
+          const double x = wp[i], y = wq[i];
+          wp[i] = c * x - sn * y;
+          wq[i] = sn * x + c * y;
+          const double u = vp[i], v = vq[i];
+          vp[i] = c * u - sn * v;
+          vq[i] = sn * u + c * v;
+        }
+      }
+    }
+  }
+  if (!done && !(worst < 1e-10))
+    return ksvd_set_error_from_host(KSVD_ENUMERIC, "Jacobi SVD did not converge");
+  std::vector<double> nrm(K);
+  for (int j = 0; j < k; ++j) {
+    double t = 0.0;
+    const double* w = col(W, j);
+    for (size_t i = 0; i < K; ++i) t += w[i] * w[i];
+    nrm[j] = std::sqrt(t);
+  }
+  std::vector<int> order(K);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return nrm[x] > nrm[y]; });
+  for (int r = 0; r < k; ++r) {
+    const int j = order[r];
+    s[r] = nrm[j];
+    const double* w = col(W, j);
+    for (size_t i = 0; i < K; ++i) {
+      U[(size_t)r * K + i] = nrm[j] > 0 ? w[i] / nrm[j] : 0.0;
+      V[(size_t)r * K + i] = Vm[(size_t)j * K + i];
+    }
+  }
+  return KSVD_OK;
+}

@@ -957,6 +957,8 @@ static int set_l2_window(ksvd_mat* M, bool on) {
   return 0;
 }
 
+static int run_steps(ksvd_run* R, int i0);
+
 static int run_loop(ksvd_run* R, const double* q1_local) {
   ksvd_mat* M = R->M;
   ksvd_ctx* c = M->ctx;
@@ -969,6 +971,13 @@ static int run_loop(ksvd_run* R, const double* q1_local) {
   TRY(enqueue_gemv_t(M, R->Q, nullptr, nullptr, nullptr, nullptr, R->z, R->st, 0, true));
   TRY(cgs(c, &R->right, R->P, R->ldp, 0, R->z, M->n, 0, false, R->eps, R->alpha + 1, R->st,
           0, ST_DEGENERATE, R->M->ctx->dprog, 1));
+  return run_steps(R, 1);
+}
+
+// GK steps i0..k_max (step i: A p_i and A^T q_{i+1} with their CGS2)
+static int run_steps(ksvd_run* R, int i0) {
+  ksvd_mat* M = R->M;
+  ksvd_ctx* c = M->ctx;
   // Pacing: the host enqueues step i only once step i-kLag has finished.
   // KSVD_PACE=spin polls the mapped progress word; the default waits on a
   // ring of events (which also flushes the launch queue).  Either way the
@@ -981,9 +990,9 @@ static int run_loop(ksvd_run* R, const double* q1_local) {
   static const bool dbg = getenv("KSVD_DEBUG_HOST") != nullptr;
   using clk = std::chrono::steady_clock;
   double t_launch = 0, t_wait = 0;
-  for (int i = 1; i <= R->k_max; ++i) {
+  for (int i = i0; i <= R->k_max; ++i) {
     auto t0 = clk::now();
-    if (i > kLag) {
+    if (i - i0 >= kLag) {
       const int s = i - kLag;
       if (spin_mode) {
         for (int spin = 0;; ++spin) {
@@ -1992,6 +2001,125 @@ int ksvd_ritz(ksvd_run* R, const double* G, const double* sigma, int take, int o
   }
   CK(cudaStreamSynchronize(c->stream));
   *n_good = good;
+  return 0;
+}
+
+int ksvd_run_restart(ksvd_run* R, int l, const double* X, const double* Y, int k_new) {
+  ksvd_mat* M = R->M;
+  ksvd_ctx* c = M->ctx;
+  CK(cudaSetDevice(c->device));
+  const int k = R->kprime;
+  if (R->status != ST_RUNNING || k != R->k_max)
+    return set_err(KSVD_ECONFIG, "restart needs a run that completed its %d steps", R->k_max);
+  if (l < 0 || l >= k) return set_err(KSVD_ECONFIG, "restart keeps l=%d of k=%d", l, k);
+  if (k_new <= l || k_new > std::min(M->m, M->n))
+    return set_err(KSVD_ECONFIG, "restart size %d outside (%d, %lld]", k_new, l,
+                   (long long)std::min(M->m, M->n));
+  if (l > 0 && (!X || !Y)) return set_err(KSVD_ECONFIG, "null restart combination");
+  cudaStream_t s = c->stream;
+  double *Xd = nullptr, *Yd = nullptr, *Qt = nullptr, *Pt = nullptr;
+  auto release = [&] {
+    for (double* p : {Xd, Yd, Qt, Pt})
+      if (p) cudaFreeAsync(p, s);
+  };
+  const size_t nl = (size_t)std::max(l, 1);
+  cudaError_t e = cudaSuccess;
+  auto ok = [&](cudaError_t x) {
+    if (e == cudaSuccess) e = x;
+  };
+  ok(cudaMallocAsync(&Xd, sizeof(double) * k * nl, s));
+  ok(cudaMallocAsync(&Yd, sizeof(double) * k * nl, s));
+  ok(cudaMallocAsync(&Qt, sizeof(double) * R->ldq * (l + 1), s));
+  ok(cudaMallocAsync(&Pt, sizeof(double) * R->ldp * nl, s));
+  if (e == cudaSuccess && l > 0) {
+    ok(cudaMemcpyAsync(Xd, X, sizeof(double) * k * l, cudaMemcpyHostToDevice, s));
+    ok(cudaMemcpyAsync(Yd, Y, sizeof(double) * k * l, cudaMemcpyHostToDevice, s));
+  }
+  if (e != cudaSuccess) {
+    release();
+    return set_err(KSVD_ERUNTIME, "restart: %s", cudaGetErrorString(e));
+  }
+  int rc = 0;
+  // Ritz combinations of the current bases, then q_{k+1} as column l
+  if (l > 0) {
+    if (M->mloc > 0)
+      rc = launch(c, KC_OTHER, k_basis_combine,
+                  dim3((unsigned)cdiv(M->mloc, kThreads), (unsigned)cdiv(l, kTT)), dim3(kThreads),
+                  0, (const double*)R->Q, R->ldq, M->mloc, k, (const double*)Xd, l, Qt, R->ldq);
+    if (!rc)
+      rc = launch(c, KC_OTHER, k_basis_combine,
+                  dim3((unsigned)cdiv(M->n, kThreads), (unsigned)cdiv(l, kTT)), dim3(kThreads), 0,
+                  (const double*)R->P, R->ldp, M->n, k, (const double*)Yd, l, Pt, R->ldp);
+  }
+  if (!rc) {
+    ok(cudaMemcpyAsync(Qt + (size_t)l * R->ldq, R->Q + (size_t)k * R->ldq,
+                       sizeof(double) * R->ldq, cudaMemcpyDeviceToDevice, s));
+    ok(cudaMemcpyAsync(R->Q, Qt, sizeof(double) * R->ldq * (l + 1), cudaMemcpyDeviceToDevice, s));
+    if (l > 0)
+      ok(cudaMemcpyAsync(R->P, Pt, sizeof(double) * R->ldp * l, cudaMemcpyDeviceToDevice, s));
+    if (e != cudaSuccess) rc = set_err(KSVD_ERUNTIME, "restart: %s", cudaGetErrorString(e));
+  }
+  release();
+  if (rc) return rc;
+  // room for k_new steps: scalars are re-allocated, bases grow on demand
+  if (k_new > R->k_max) {
+    for (double* p : {R->alpha, R->beta}) CK(cudaFreeAsync(p, s));
+    CK(cudaMallocAsync(&R->alpha, sizeof(double) * (k_new + 2), s));
+    CK(cudaMallocAsync(&R->beta, sizeof(double) * (k_new + 3), s));
+  }
+  R->k_max = k_new;
+  CK(cudaMemsetAsync(R->alpha, 0, sizeof(double) * (k_new + 2), s));
+  CK(cudaMemsetAsync(R->beta, 0, sizeof(double) * (k_new + 3), s));
+  CK(cudaMemsetAsync(R->st, 0, sizeof(DevState), s));
+  c->hprog->prog = -1;
+  c->hprog->halt_step = INT_MAX;
+  c->hprog->status = 0;
+  TRY(set_l2_window(M, true));
+  // z = A^T q_{l+1}; CGS2 against the l kept right Ritz vectors (the spike);
+  // alpha_{l+1} < eps: the kept space is invariant (k' = l)
+  TRY(enqueue_gemv_t(M, R->Q + (size_t)l * R->ldq, nullptr, nullptr, nullptr, nullptr, R->z,
+                     R->st, l, true));
+  TRY(cgs(c, &R->right, R->P, R->ldp, l, R->z, M->n, l > 0 ? R->reorth : 0, false, R->eps,
+          R->alpha + l + 1, R->st, l, l > 0 ? ST_ALPHA_BREAK : ST_DEGENERATE, c->dprog, 1));
+  return run_steps(R, l + 1);
+}
+
+int ksvd_run_ritz_bases(ksvd_run* R, const double* X, int kq, const double* Y, int kp, int take,
+                        double* U, double* V) {
+  ksvd_mat* M = R->M;
+  ksvd_ctx* c = M->ctx;
+  CK(cudaSetDevice(c->device));
+  if (take <= 0) return take == 0 ? 0 : set_err(KSVD_ECONFIG, "take %d", take);
+  if (kq < 1 || kq > R->cap + 1 || kp < 1 || kp > R->cap)
+    return set_err(KSVD_ECONFIG, "basis columns kq=%d kp=%d outside the run", kq, kp);
+  cudaStream_t s = c->stream;
+  const int64_t ldu = M->m_pad, ldv = M->n_pad;
+  for (double* p : {R->G, R->V, R->U, R->sig})
+    if (p) cudaFreeAsync(p, s);
+  R->G = R->V = R->U = R->sig = nullptr;
+  CK(cudaMallocAsync(&R->G, sizeof(double) * ((size_t)kq + kp) * take, s));
+  CK(cudaMallocAsync(&R->V, sizeof(double) * ldv * take, s));
+  CK(cudaMallocAsync(&R->U, sizeof(double) * ldu * take, s));
+  CK(cudaMemsetAsync(R->U, 0, sizeof(double) * ldu * take, s));
+  double* Xd = R->G;
+  double* Yd = R->G + (size_t)kq * take;
+  CK(cudaMemcpyAsync(Xd, X, sizeof(double) * kq * take, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(Yd, Y, sizeof(double) * kp * take, cudaMemcpyHostToDevice, s));
+  if (M->mloc > 0)
+    TRY(launch(c, KC_OTHER, k_basis_combine,
+               dim3((unsigned)cdiv(M->mloc, kThreads), (unsigned)cdiv(take, kTT)), dim3(kThreads),
+               0, (const double*)R->Q, R->ldq, M->mloc, kq, (const double*)Xd, take, R->U, ldu));
+  TRY(launch(c, KC_OTHER, k_basis_combine,
+             dim3((unsigned)cdiv(M->n, kThreads), (unsigned)cdiv(take, kTT)), dim3(kThreads), 0,
+             (const double*)R->P, R->ldp, M->n, kp, (const double*)Yd, take, R->V, ldv));
+  TRY(launch(c, KC_OTHER, k_fix_signs, dim3(take), dim3(kThreads), 0, R->V, ldv, M->n, R->U,
+             ldu, M->mloc));
+  if (M->mloc > 0)
+    CK(cudaMemcpy2DAsync(U, sizeof(double) * M->mloc, R->U, sizeof(double) * ldu,
+                         sizeof(double) * M->mloc, take, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpy2DAsync(V, sizeof(double) * M->n, R->V, sizeof(double) * ldv,
+                       sizeof(double) * M->n, take, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
   return 0;
 }
 

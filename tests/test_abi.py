@@ -105,3 +105,21 @@ def test_bidiag_sv2_relative_accuracy():
         assert np.all(np.abs(got - ref)[tail] / ref[tail] < 1e-14), (k, graded)
         # head: QL on B^T B, like the reference (absolute eps*theta_1)
         assert np.max(np.abs(got - ref)[~tail]) < 1e-13 * ref[0], (k, graded)
+
+
+def test_dense_svd_native_matches_numpy():
+    """ksvd_dense_svd (host Jacobi, restarted mode's projected matrix)."""
+    from paper_2104_10785_b200.restart import dense_svd
+    rng = np.random.default_rng(3)
+    for k in (1, 2, 7, 40, 120):
+        T = np.triu(rng.standard_normal((k, k)))
+        T[: k // 3, : k // 3] = np.diag(np.sort(rng.uniform(1, 5, k // 3))[::-1])
+        Uh, s, Vh = dense_svd(T)
+        ref = np.linalg.svd(T, compute_uv=False)
+        assert np.allclose(s, ref, rtol=1e-13, atol=1e-15 * ref[0])
+        assert np.allclose(Uh * s @ Vh.T, T, atol=1e-13 * ref[0])
+        assert np.allclose(Vh.T @ Vh, np.eye(k), atol=1e-13)
+    # graded: tiny singular values to high relative accuracy
+    T = np.diag(10.0 ** -np.arange(0, 16, 2.0)) @ np.triu(np.ones((8, 8)) * 0.1 + np.eye(8))
+    s = dense_svd(T)[1]
+    assert np.all(s > 0) and s[-1] < 1e-13
