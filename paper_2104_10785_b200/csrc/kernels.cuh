@@ -1565,29 +1565,6 @@ k_scale(const double* __restrict__ src, const double* __restrict__ scale,
 // ---------------------------------------------------------------------------
 // Ritz assembly (fsvd.py:191-194)
 
-// V[:, t] = sum_j G[j + t*kp] P[:, j]   (P: n rows, ldp; V: ldv)
-constexpr int kTT = 8;
-__global__ void __launch_bounds__(kThreads)
-k_basis_combine(const double* __restrict__ P, int64_t ldp, int64_t n, int kp,
-                const double* __restrict__ G, int take, double* __restrict__ V,
-                int64_t ldv) {
-  const int64_t r = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  const int t0 = blockIdx.y * kTT;
-  if (r >= n) return;
-  double acc[kTT];
-#pragma unroll
-  for (int tt = 0; tt < kTT; ++tt) acc[tt] = 0.0;
-  for (int j = 0; j < kp; ++j) {
-    const double pj = P[(int64_t)j * ldp + r];
-#pragma unroll
-    for (int tt = 0; tt < kTT; ++tt)
-      if (t0 + tt < take) acc[tt] = fma(pj, __ldg(G + j + (int64_t)(t0 + tt) * kp), acc[tt]);
-  }
-#pragma unroll
-  for (int tt = 0; tt < kTT; ++tt)
-    if (t0 + tt < take) V[(int64_t)(t0 + tt) * ldv + r] = acc[tt];
-}
-
 // Y[:, t] = (A X[:, t]) / sigma[t] on the FP64 tensor cores (DMMA,
 // mma.sync.m8n8k4.f64): one pass over A for up to 32 right-hand sides per
 // CTA column (the reference runs `take` separate matvecs, fsvd.py:193-194).
@@ -1759,6 +1736,66 @@ k_fix_signs(double* __restrict__ V, int64_t ldv, int64_t n,
   for (int64_t i = tid; i < n; i += kThreads) v[i] *= s;
   double* u = U + (int64_t)j * ldu;
   for (int64_t i = tid; i < mloc; i += kThreads) u[i] *= s;
+}
+
+
+// Y[:, t] = sum_j B[:, j] G[j + t*kp] on the FP64 tensor cores: the
+// tall-skinny Ritz / restart contractions V = P G, U = Q X (north star (c);
+// fsvd.py:191).  B is a column-major basis (ldb), L rows x kp columns; G is
+// kp x take column-major.  CTA = 8 warps x 32 rows, 32 output columns
+// (grid.y tiles take); warp tile 32 x 32 = 4 x 4 m8n8 accumulators; per
+// k-step of 4, each lane loads 4 basis elements (4 columns x 8 consecutive
+// rows per load instruction: full 32-byte sectors) and 4 G elements (L1),
+// and issues 16 DMMAs.  Fixed k order: deterministic.
+constexpr int kBCR = 32 * kWarps;  // rows per CTA
+__global__ void __launch_bounds__(kThreads)
+k_basis_combine_dmma(const double* __restrict__ B, int64_t ldb, int64_t L, int kp,
+                     const double* __restrict__ G, int take, double* __restrict__ Y,
+                     int64_t ldy) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gi = lane >> 2, ti = lane & 3;
+  const int64_t rw = (int64_t)blockIdx.x * kBCR + warp * 32;
+  const int t0 = blockIdx.y * 32;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  bool rok[4];
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) rok[mt] = rw + mt * 8 + gi < L;
+  bool cok[4];
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) cok[nt] = t0 + nt * 8 + gi < take;
+#pragma unroll 4
+  for (int j0 = 0; j0 < kp; j0 += 4) {
+    const int j = j0 + ti;
+    const bool jok = j < kp;
+    double av[4], bv[4];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+      av[mt] = (jok && rok[mt]) ? __ldg(B + (int64_t)j * ldb + rw + mt * 8 + gi) : 0.0;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+      bv[nt] = (jok && cok[nt]) ? __ldg(G + j + (int64_t)(t0 + nt * 8 + gi) * kp) : 0.0;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) dmma_8x8x4(acc[mt][nt], av[mt], bv[nt]);
+  }
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) {
+    const int64_t r = rw + mt * 8 + gi;
+    if (r >= L) continue;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int t = t0 + nt * 8 + 2 * ti + h;
+        if (t < take) Y[(int64_t)t * ldy + r] = acc[mt][nt][h];
+      }
+    }
+  }
 }
 
 }  // namespace ksvd

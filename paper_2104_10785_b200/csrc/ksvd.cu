@@ -1043,6 +1043,15 @@ static int run_steps(ksvd_run* R, int i0) {
   return read_state(R);
 }
 
+// Y = B[:, :kp] G (k_basis_combine_dmma): Ritz vectors and restart bases
+static int basis_combine(ksvd_ctx* c, const double* B, int64_t ldb, int64_t L, int kp,
+                         const double* G, int take, double* Y, int64_t ldy) {
+  if (L <= 0 || take <= 0) return 0;
+  return launch(c, KC_OTHER, k_basis_combine_dmma,
+                dim3((unsigned)cdiv(L, kBCR), (unsigned)cdiv(take, 32)), dim3(kThreads), 0, B, ldb,
+                L, kp, G, take, Y, ldy);
+}
+
 template <typename TA>
 static int enqueue_multi_rhs(ksvd_mat* M, const double* X, int64_t ldx, int k,
                              const double* sigma, double* Y, int64_t ldy) {
@@ -1965,9 +1974,7 @@ int ksvd_ritz(ksvd_run* R, const double* G, const double* sigma, int take, int o
   CK(cudaMemcpyAsync(R->G, G, sizeof(double) * kp * take, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(R->sig, sigma, sizeof(double) * take, cudaMemcpyHostToDevice, c->stream));
   // V = P[:, :k'] G  (fsvd.py:191)
-  TRY(launch(c, KC_OTHER, k_basis_combine, dim3((unsigned)cdiv(M->n, kThreads), (unsigned)cdiv(take, kTT)),
-             dim3(kThreads), 0, (const double*)R->P, R->ldp, M->n, kp, (const double*)R->G, take,
-             R->V, ldv));
+  TRY(basis_combine(c, R->P, R->ldp, M->n, kp, R->G, take, R->V, ldv));
   // U[:, t] = A V[:, t] / sigma_t, one pass over A (fsvd.py:192-194)
   TRY(multi_rhs(M, R->V, ldv, take, R->sig, R->U, ldu));
   int good = take;
@@ -2042,14 +2049,8 @@ int ksvd_run_restart(ksvd_run* R, int l, const double* X, const double* Y, int k
   int rc = 0;
   // Ritz combinations of the current bases, then q_{k+1} as column l
   if (l > 0) {
-    if (M->mloc > 0)
-      rc = launch(c, KC_OTHER, k_basis_combine,
-                  dim3((unsigned)cdiv(M->mloc, kThreads), (unsigned)cdiv(l, kTT)), dim3(kThreads),
-                  0, (const double*)R->Q, R->ldq, M->mloc, k, (const double*)Xd, l, Qt, R->ldq);
-    if (!rc)
-      rc = launch(c, KC_OTHER, k_basis_combine,
-                  dim3((unsigned)cdiv(M->n, kThreads), (unsigned)cdiv(l, kTT)), dim3(kThreads), 0,
-                  (const double*)R->P, R->ldp, M->n, k, (const double*)Yd, l, Pt, R->ldp);
+    rc = basis_combine(c, R->Q, R->ldq, M->mloc, k, Xd, l, Qt, R->ldq);
+    if (!rc) rc = basis_combine(c, R->P, R->ldp, M->n, k, Yd, l, Pt, R->ldp);
   }
   if (!rc) {
     ok(cudaMemcpyAsync(Qt + (size_t)l * R->ldq, R->Q + (size_t)k * R->ldq,
@@ -2105,13 +2106,8 @@ int ksvd_run_ritz_bases(ksvd_run* R, const double* X, int kq, const double* Y, i
   double* Yd = R->G + (size_t)kq * take;
   CK(cudaMemcpyAsync(Xd, X, sizeof(double) * kq * take, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(Yd, Y, sizeof(double) * kp * take, cudaMemcpyHostToDevice, s));
-  if (M->mloc > 0)
-    TRY(launch(c, KC_OTHER, k_basis_combine,
-               dim3((unsigned)cdiv(M->mloc, kThreads), (unsigned)cdiv(take, kTT)), dim3(kThreads),
-               0, (const double*)R->Q, R->ldq, M->mloc, kq, (const double*)Xd, take, R->U, ldu));
-  TRY(launch(c, KC_OTHER, k_basis_combine,
-             dim3((unsigned)cdiv(M->n, kThreads), (unsigned)cdiv(take, kTT)), dim3(kThreads), 0,
-             (const double*)R->P, R->ldp, M->n, kp, (const double*)Yd, take, R->V, ldv));
+  TRY(basis_combine(c, R->Q, R->ldq, M->mloc, kq, Xd, take, R->U, ldu));
+  TRY(basis_combine(c, R->P, R->ldp, M->n, kp, Yd, take, R->V, ldv));
   TRY(launch(c, KC_OTHER, k_fix_signs, dim3(take), dim3(kThreads), 0, R->V, ldv, M->n, R->U,
              ldu, M->mloc));
   if (M->mloc > 0)
