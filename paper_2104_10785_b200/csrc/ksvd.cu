@@ -28,6 +28,7 @@
 #include "gen.cuh"
 #include "kernels.cuh"
 #include "klrm.cuh"
+#include "resident.cuh"
 #include "ksvd.h"
 
 using namespace ksvd;
@@ -1043,6 +1044,8 @@ static int run_steps(ksvd_run* R, int i0) {
   return read_state(R);
 }
 
+constexpr size_t kResidentSmemMax = 200 * 1024;  // single-CTA / resident kernels
+
 // Y = B[:, :kp] G (k_basis_combine_dmma): Ritz vectors and restart bases
 static int basis_combine(ksvd_ctx* c, const double* B, int64_t ldb, int64_t L, int kp,
                          const double* G, int take, double* Y, int64_t ldy) {
@@ -1056,6 +1059,27 @@ template <typename TA>
 static int enqueue_multi_rhs(ksvd_mat* M, const double* X, int64_t ldx, int k,
                              const double* sigma, double* Y, int64_t ldy) {
   if (M->mloc == 0 || k == 0) return 0;
+  const size_t xs_bytes = sizeof(double) * (size_t)std::min(k, 32) * ldx;
+  if (cdiv(M->mloc, kMR) * cdiv(k, kMC) < M->ctx->sms && xs_bytes <= kResidentSmemMax) {
+    // too few 256-row tiles to fill the GPU: one CTA per SM, X in shared
+    // memory, one warp per row
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(k_multi_rhs_rows<TA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)kResidentSmemMax));
+      attr = true;
+    }
+    const int64_t G = std::min<int64_t>(M->ctx->sms, cdiv(M->mloc, kWarps));
+    const int rpc = (int)cdiv(M->mloc, G);
+    for (int t0 = 0; t0 < k; t0 += 32) {
+      const int kk = std::min(32, k - t0);
+      TRY(launch(M->ctx, KC_OTHER, k_multi_rhs_rows<TA>, dim3((unsigned)cdiv(M->mloc, rpc)),
+                 dim3(kThreads), sizeof(double) * (size_t)kk * ldx, (const TA*)M->A, M->lda,
+                 M->mloc, M->n, X + (int64_t)t0 * ldx, ldx, kk,
+                 sigma ? sigma + t0 : (const double*)nullptr, Y + (int64_t)t0 * ldy, ldy, rpc));
+    }
+    return 0;
+  }
   static bool attr = false;
   if (!attr) {
     CK(cudaFuncSetAttribute(k_multi_rhs<TA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1376,6 +1400,121 @@ static int klrm_write_from(ksvd_mat* M, int fd) {
       return set_err(KSVD_ERUNTIME, "KLRM: write failed at row %lld", (long long)(M->row0 + r));
   }
   return 0;
+}
+
+// Small matrices: the whole loop as one cooperative kernel with A resident
+// in shared memory (resident.cuh).  Eligible on one rank when every CTA's
+// row block of A plus its slices of the bases fit its shared memory.
+struct ResidentPlan {
+  int G = 0, R = 0, C = 0;
+  size_t smem = 0;
+};
+
+static bool resident_plan(ksvd_run* Rn, ResidentPlan* pl) {
+  static const bool off = [] {
+    const char* e = getenv("KSVD_RESIDENT");
+    return e && strcmp(e, "0") == 0;
+  }();
+  ksvd_mat* M = Rn->M;
+  ksvd_ctx* c = M->ctx;
+  if (off || c->comm || M->fac || M->mloc != M->m) return false;
+  const int64_t G0 = std::min<int64_t>(c->sms, M->m);
+  const int64_t R = cdiv(M->m, G0);
+  const int64_t G = cdiv(M->m, R);
+  const int64_t C = cdiv(M->n, G);
+  const int64_t kq = Rn->k_max + 1;
+  // the layout of k_gk_resident's shared memory (resident.cuh)
+  size_t words = ((size_t)kq * R + (size_t)Rn->k_max * C + R + C + kq + 2 + 1) & ~(size_t)1;
+  words += (size_t)(M->n + 1) & ~(size_t)1;
+  words += (((size_t)(kq + 1) * G + 1) & ~(size_t)1) + 2;
+  const size_t smem = sizeof(double) * words + (size_t)R * M->n * esize(M->dtype);
+  if (smem > kResidentSmemMax) return false;
+  pl->G = (int)G;
+  pl->R = (int)R;
+  pl->C = (int)C;
+  pl->smem = smem;
+  return true;
+}
+
+template <typename TA>
+static int resident_attr() {
+  static bool done = false;
+  if (!done) {
+    CK(cudaFuncSetAttribute(k_gk_resident<TA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kResidentSmemMax));
+    done = true;
+  }
+  return 0;
+}
+
+static int run_resident(ksvd_run* Rn, const ResidentPlan& pl, const double* q1_local) {
+  ksvd_mat* M = Rn->M;
+  ksvd_ctx* c = M->ctx;
+  cudaStream_t s = c->stream;
+  TRY(grow_bases(Rn, Rn->k_max));
+  CK(cudaMemcpyAsync(Rn->Q, q1_local, sizeof(double) * M->mloc, cudaMemcpyHostToDevice, s));
+  ResArgs a{};
+  a.A = M->A;
+  a.lda = M->lda;
+  a.m = M->m;
+  a.n = M->n;
+  a.k_max = Rn->k_max;
+  a.passes = Rn->reorth;
+  a.eps = Rn->eps;
+  a.R = pl.R;
+  a.C = pl.C;
+  a.kq = Rn->k_max + 1;
+  a.Q = Rn->Q;
+  a.P = Rn->P;
+  a.ldq = Rn->ldq;
+  a.ldp = Rn->ldp;
+  a.alpha = Rn->alpha;
+  a.beta = Rn->beta;
+  a.w_out = Rn->w;
+  a.st = Rn->st;
+  a.tdbg = c->tdbg;
+  const size_t part_elems = 2 * (((size_t)(a.kq + 1) * pl.G + 1) & ~(size_t)1) + 2;
+  const size_t z_elems = (size_t)pl.G * M->n;
+  double* buf = nullptr;
+  CK(cudaMallocAsync(&buf, sizeof(double) * (M->n_pad + part_elems + z_elems), s));
+  a.pvec = buf;
+  a.part = buf + M->n_pad;
+  a.zpart = a.part + part_elems;
+  void* args[] = {&a};
+  const void* kern;
+  if (M->dtype == KSVD_F32) {
+    TRY(resident_attr<float>());
+    kern = (const void*)k_gk_resident<float>;
+  } else {
+    TRY(resident_attr<double>());
+    kern = (const void*)k_gk_resident<double>;
+  }
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->profiling) {
+    TRY(get_event(c, &e0));
+    TRY(get_event(c, &e1));
+    CK(cudaEventRecord(e0, s));
+  }
+  const cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3((unsigned)pl.G), dim3(kThreads),
+                                                     args, pl.smem, s);
+  cudaFreeAsync(buf, s);
+  if (e != cudaSuccess)
+    return set_err(KSVD_ERUNTIME, "resident GK launch: %s", cudaGetErrorString(e));
+  if (c->profiling) {
+    CK(cudaEventRecord(e1, s));
+    c->pending.push_back({e0, e1, KC_CGS});
+  }
+  c->launches++;
+  if (c->tdbg) {
+    unsigned long long t[8];
+    CK(cudaMemcpyAsync(t, c->tdbg, sizeof t, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    fprintf(stderr, "[ksvd] resident phases (us, CTA 0, cumulative): load %.1f gemv_n %.1f "
+            "cgs_left %.1f gemv_t %.1f cgs_right %.1f publish %.1f\n", t[0] * 1e-3, t[1] * 1e-3,
+            t[2] * 1e-3, t[3] * 1e-3, t[4] * 1e-3, t[5] * 1e-3);
+    CK(cudaMemsetAsync(c->tdbg, 0, sizeof t, s));
+  }
+  return read_state(Rn);
 }
 
 // ---------------------------------------------------------------------------
@@ -1877,7 +2016,8 @@ int ksvd_gk_run(ksvd_mat* M, int k_max, double eps, int reorth, const double* q1
   c->hprog->halt_step = INT_MAX;
   c->hprog->status = 0;
 #undef RUN_CK
-  int rc = run_loop(R, q1_local);
+  ResidentPlan pl;
+  int rc = resident_plan(R, &pl) ? run_resident(R, pl, q1_local) : run_loop(R, q1_local);
   if (rc) return fail(rc);
   *out = R;
   return 0;
@@ -1978,7 +2118,25 @@ int ksvd_ritz(ksvd_run* R, const double* G, const double* sigma, int take, int o
   // U[:, t] = A V[:, t] / sigma_t, one pass over A (fsvd.py:192-194)
   TRY(multi_rhs(M, R->V, ldv, take, R->sig, R->U, ldu));
   int good = take;
-  if (ortho) {
+  const int ldm = (int)rup(std::max<int64_t>(M->mloc, 1), 2);
+  const size_t uf_smem = sizeof(double) * ((size_t)take * ldm + take);
+  if (ortho && c->comm == nullptr && uf_smem <= kResidentSmemMax) {
+    // the same filter in one single-CTA launch (U fits shared memory)
+    TRY(reset_state(c, R->st_aux));
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(k_ufilter_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)kResidentSmemMax));
+      attr = true;
+    }
+    TRY(launch(c, KC_OTHER, k_ufilter_small, dim3(1), dim3(kUfThreads), uf_smem, R->U, ldu,
+               (int)M->mloc, take, ldm, 1e-2, R->st_aux));
+    DevState h{};
+    CK(cudaMemcpyAsync(&h, R->st_aux, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (h.status == ST_NONFINITE) return set_err(KSVD_ENUMERIC, "non-finite Ritz vectors");
+    if (h.status == ST_CUT) good = h.kprime;
+  } else if (ortho) {
     // CGS2 column filter, cut at the first residual < 1e-2 (fsvd.py:145-155)
     TRY(reset_state(c, R->st_aux));
     const unsigned g = (unsigned)cdiv(std::max<int64_t>(M->mloc, 1), kThreads);

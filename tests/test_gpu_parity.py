@@ -277,13 +277,17 @@ print(json.dumps(out))
 """
 
 
-@pytest.mark.parametrize("env", [{"KSVD_TILE": "0"}, {"KSVD_COOP": "0"}, {"KSVD_FORCE_NCCL": "1"},
-                                 {"KSVD_COOP_GLOBAL": "1", "KSVD_TILE": "0"},
-                                 {"KSVD_CGS_SYNC": "5"}, {"KSVD_RED_MAX": "0"},
-                                 {"KSVD_RED_MAX": "100000000"}, {"KSVD_PDL": "0"},
-                                 {"KSVD_PDL_TRIG": "3"}, {}])
+_MULTI = {"KSVD_RESIDENT": "0"}  # small cases would otherwise take the resident kernel
+
+
+@pytest.mark.parametrize("env", [{"KSVD_TILE": "0", **_MULTI}, {"KSVD_COOP": "0", **_MULTI},
+                                 {"KSVD_FORCE_NCCL": "1"},
+                                 {"KSVD_COOP_GLOBAL": "1", "KSVD_TILE": "0", **_MULTI},
+                                 {"KSVD_CGS_SYNC": "5", **_MULTI}, {"KSVD_RED_MAX": "0", **_MULTI},
+                                 {"KSVD_RED_MAX": "100000000", **_MULTI}, {"KSVD_PDL": "0", **_MULTI},
+                                 {"KSVD_PDL_TRIG": "3", **_MULTI}, _MULTI, {}])
 def test_cgs_paths_agree(env):
-    """The tile-resident (2-round k_cgs2_tile2 with redundant or distributed
+    """The whole-loop resident kernel (small matrices, default), the tile-resident (2-round k_cgs2_tile2 with redundant or distributed
     reductions, 5-round k_cgs2_tile), global-load cooperative and
     multi-kernel CGS2 paths (selected at load time) all meet the parity bar,
     with and without programmatic dependent launch; KSVD_FORCE_NCCL runs the
