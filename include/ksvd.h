@@ -85,7 +85,8 @@ int ksvd_ctx_sync(ksvd_ctx *ctx);
 /* Per-kernel-class device timing (CUDA events on the launching stream). */
 int ksvd_ctx_set_profiling(ksvd_ctx *ctx, int on);
 /* cls: 0 gemv_n (A p), 1 gemv_t (A^T q), 2 CGS2 + norms, 3 other,
- * 4 product finalisation (split sums, axpy); returns launches and ms */
+ * 4 product finalisation (split sums, axpy), 5 whole-loop resident kernel
+ * (small matrices); returns launches and ms */
 int ksvd_ctx_kernel_stats(ksvd_ctx *ctx, int cls, int64_t *launches,
                           double *ms);
 int ksvd_ctx_reset_stats(ksvd_ctx *ctx);

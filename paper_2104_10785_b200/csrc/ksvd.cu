@@ -74,7 +74,9 @@ static inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
 
 // ---------------------------------------------------------------------------
 // context
-enum KClass { KC_GEMV_N = 0, KC_GEMV_T = 1, KC_CGS = 2, KC_OTHER = 3, KC_FIN = 4, KC_NUM = 5 };
+enum KClass {
+  KC_GEMV_N = 0, KC_GEMV_T = 1, KC_CGS = 2, KC_OTHER = 3, KC_FIN = 4, KC_RESIDENT = 5, KC_NUM = 6
+};
 
 struct ksvd_ctx {
   int device = 0, rank = 0, nranks = 1, sms = 148;
@@ -1502,7 +1504,7 @@ static int run_resident(ksvd_run* Rn, const ResidentPlan& pl, const double* q1_l
     return set_err(KSVD_ERUNTIME, "resident GK launch: %s", cudaGetErrorString(e));
   if (c->profiling) {
     CK(cudaEventRecord(e1, s));
-    c->pending.push_back({e0, e1, KC_CGS});
+    c->pending.push_back({e0, e1, KC_RESIDENT});
   }
   c->launches++;
   if (c->tdbg) {
