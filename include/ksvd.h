@@ -231,6 +231,11 @@ int ksvd_bidiag_sv2(int k, const double *alphas, const double *betas, double *th
  * high relative accuracy).  No reference counterpart: SURVEY.md 8(f) row 3
  * (Ritz-vector restarts are a non-goal of the reference). */
 int ksvd_dense_svd(int k, const double *T, double *U, double *s, double *V);
+/* The same SVD in one CTA on the device (parallel round-robin Jacobi, the
+ * north star's "single-CTA kernel" option); falls back to the host routine
+ * when 2 k^2 doubles exceed the CTA's shared memory. */
+int ksvd_dense_svd_dev(ksvd_ctx *ctx, int k, const double *T, double *U, double *s,
+                       double *V);
 
 #ifdef __cplusplus
 }

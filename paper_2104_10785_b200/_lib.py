@@ -79,6 +79,7 @@ SIGNATURES = {
     "ksvd_matrix_from_klrm": (C.c_int, [_vp, C.c_char_p, C.c_int, C.POINTER(_vp)]),
     "ksvd_matrix_to_klrm": (C.c_int, [_vp, C.c_char_p]),
     "ksvd_dense_svd": (C.c_int, [C.c_int, _pd, _pd, _pd, _pd]),
+    "ksvd_dense_svd_dev": (C.c_int, [_vp, C.c_int, _pd, _pd, _pd, _pd]),
     "ksvd_run_restart": (C.c_int, [_vp, C.c_int, _pd, _pd, C.c_int]),
     "ksvd_run_ritz_bases": (C.c_int, [_vp, _pd, C.c_int, _pd, C.c_int, C.c_int, _pd, _pd]),
     "ksvd_matrix_from_factors": (C.c_int, [_vp, _pd, _pd, _pd, C.c_int64, C.c_int64, C.c_int64,

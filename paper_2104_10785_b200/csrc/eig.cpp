@@ -237,19 +237,27 @@ extern "C" int ksvd_dense_svd(int k, const double* T, double* U, double* s, doub
   const double zero2 = fro2 * DBL_EPSILON * DBL_EPSILON;
   bool done = false;
   double worst = 0.0;
+  std::vector<double> d(K);  // squared column norms, updated through the rotations
   for (int sweep = 0; sweep < 80 && !done; ++sweep) {
     done = true;
     worst = 0.0;
+    for (int j = 0; j < k; ++j) {  // refreshed every sweep (no drift)
+      const double* w = col(W, j);
+      double t = 0.0;
+      for (size_t i = 0; i < K; ++i) t += w[i] * w[i];
+      d[j] = t;
+    }
     for (int p = 0; p < k - 1; ++p) {
       for (int q = p + 1; q < k; ++q) {
-        double* wp = col(W, p);
-        double* wq = col(W, q);
-        double a = 0.0, b = 0.0, g = 0.0;
-        for (size_t i = 0; i < K; ++i) {
-          a += wp[i] * wp[i];
-          b += wq[i] * wq[i];
-          g += wp[i] * wq[i];
-        }
+        double* __restrict__ wp = col(W, p);
+        double* __restrict__ wq = col(W, q);
+        const double a = d[p], b = d[q];
+        double g4[4] = {0.0, 0.0, 0.0, 0.0};  // 4 independent chains (fixed order)
+        size_t i4 = 0;
+        for (; i4 + 4 <= K; i4 += 4)
+          for (int u = 0; u < 4; ++u) g4[u] += wp[i4 + u] * wq[i4 + u];
+        for (; i4 < K; ++i4) g4[0] += wp[i4] * wq[i4];
+        const double g = (g4[0] + g4[1]) + (g4[2] + g4[3]);
         if (g == 0.0 || a <= zero2 || b <= zero2 || std::fabs(g) <= tol * std::sqrt(a * b))
           continue;
         worst = std::max(worst, std::fabs(g) / std::sqrt(a * b));
@@ -257,8 +265,8 @@ extern "C" int ksvd_dense_svd(int k, const double* T, double* U, double* s, doub
         const double zeta = (b - a) / (2.0 * g);
         const double t = (zeta >= 0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
         const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
-        double* vp = col(Vm, p);
-        double* vq = col(Vm, q);
+        double* __restrict__ vp = col(Vm, p);
+        double* __restrict__ vq = col(Vm, q);
         for (size_t i = 0; i < K; ++i) {
           const double x = wp[i], y = wq[i];
           wp[i] = c * x - sn * y;
@@ -267,6 +275,8 @@ extern "C" int ksvd_dense_svd(int k, const double* T, double* U, double* s, doub
           vp[i] = c * u - sn * v;
           vq[i] = sn * u + c * v;
         }
+        d[p] = a - t * g;  // exact for the rotation that zeroes the pair
+        d[q] = b + t * g;
       }
     }
   }

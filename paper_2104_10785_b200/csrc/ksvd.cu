@@ -1449,13 +1449,18 @@ static int resident_attr() {
   return 0;
 }
 
-static int run_resident(ksvd_run* Rn, const ResidentPlan& pl, const double* q1_local) {
+// q1_local: the start vector (fresh run, l = 0), or nullptr to resume after
+// a restart with Q[:, :l+1] and P[:, :l] already in place
+static int run_resident(ksvd_run* Rn, const ResidentPlan& pl, const double* q1_local,
+                        int l = 0) {
   ksvd_mat* M = Rn->M;
   ksvd_ctx* c = M->ctx;
   cudaStream_t s = c->stream;
   TRY(grow_bases(Rn, Rn->k_max));
-  CK(cudaMemcpyAsync(Rn->Q, q1_local, sizeof(double) * M->mloc, cudaMemcpyHostToDevice, s));
+  if (q1_local)
+    CK(cudaMemcpyAsync(Rn->Q, q1_local, sizeof(double) * M->mloc, cudaMemcpyHostToDevice, s));
   ResArgs a{};
+  a.l = l;
   a.A = M->A;
   a.lda = M->lda;
   a.m = M->m;
@@ -1896,6 +1901,40 @@ int ksvd_matrix_from_factors(ksvd_ctx* c, const double* left_rows, const double*
   return 0;
 }
 
+int ksvd_dense_svd_dev(ksvd_ctx* c, int k, const double* T, double* U, double* s, double* V) {
+  if (k <= 0) return set_err(KSVD_ECONFIG, "empty matrix");
+  const int kk = (k + 1) & ~1;
+  const size_t smem = sizeof(double) * (2 * (size_t)kk * k + kk);
+  if (smem > kResidentSmemMax) return ksvd_dense_svd(k, T, U, s, V);  // host Jacobi
+  CK(cudaSetDevice(c->device));
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_dense_svd_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kResidentSmemMax));
+    attr = true;
+  }
+  cudaStream_t st = c->stream;
+  const size_t kk2 = (size_t)k * k;
+  double* buf = nullptr;
+  CK(cudaMallocAsync(&buf, sizeof(double) * (3 * kk2 + k) + sizeof(int) * 2, st));
+  double *Td = buf, *Ud = buf + kk2, *Vd = buf + 2 * kk2, *sd = buf + 3 * kk2;
+  int* info = reinterpret_cast<int*>(sd + k);
+  CK(cudaMemcpyAsync(Td, T, sizeof(double) * kk2, cudaMemcpyHostToDevice, st));
+  int rc = launch(c, KC_OTHER, k_dense_svd_cta, dim3(1), dim3(kSvdThreads), smem, k,
+                  (const double*)Td, Ud, sd, Vd, info);
+  int sweeps = 0;
+  if (!rc) {
+    CK(cudaMemcpyAsync(U, Ud, sizeof(double) * kk2, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(V, Vd, sizeof(double) * kk2, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(s, sd, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&sweeps, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+  }
+  cudaFreeAsync(buf, st);
+  CK(cudaStreamSynchronize(st));
+  if (!rc && sweeps >= 80) rc = set_err(KSVD_ENUMERIC, "Jacobi SVD did not converge");
+  return rc;
+}
+
 int ksvd_matrix_free(ksvd_mat* M) { return free_matrix(M); }
 
 int ksvd_matrix_shape(ksvd_mat* M, int64_t* m, int64_t* n, int64_t* row0, int64_t* mloc,
@@ -2235,6 +2274,8 @@ int ksvd_run_restart(ksvd_run* R, int l, const double* X, const double* Y, int k
   c->hprog->prog = -1;
   c->hprog->halt_step = INT_MAX;
   c->hprog->status = 0;
+  ResidentPlan pl;
+  if (resident_plan(R, &pl)) return run_resident(R, pl, nullptr, l);
   TRY(set_l2_window(M, true));
   // z = A^T q_{l+1}; CGS2 against the l kept right Ritz vectors (the spike);
   // alpha_{l+1} < eps: the kept space is invariant (k' = l)

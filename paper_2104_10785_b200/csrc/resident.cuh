@@ -17,6 +17,7 @@
 // the residual left in R->w are those of the multi-kernel loop
 // (bidiag.py:111-178), so ksvd_run_info / _extend / _ritz work unchanged.
 #pragma once
+#include <cfloat>
 #include <cooperative_groups.h>
 
 namespace ksvd {
@@ -25,6 +26,7 @@ struct ResArgs {
   const void* A;
   int64_t lda, m, n;
   int k_max, passes;
+  int l;  // resume after a thick restart: Q[:, :l+1], P[:, :l] preloaded (0: fresh run)
   double eps;
   int R, C;  // rows / right-basis rows per CTA
   int kq;    // Q columns held in smem (k_max + 1)
@@ -112,7 +114,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_gk_resident(ResArgs a) {
       const int64_t r = e / n, c = e - r * n;
       As[e] = Ag[r * a.lda + c];
     }
-    for (int r = tid; r < nr; r += kThreads) Qs[r] = a.Q[r0 + r];
+    for (int j = 0; j <= a.l; ++j)
+      for (int r = tid; r < nr; r += kThreads) Qs[(size_t)j * R + r] = a.Q[(int64_t)j * a.ldq + r0 + r];
+    for (int j = 0; j < a.l; ++j)
+      for (int cc = tid; cc < nc; cc += kThreads) Ps[(size_t)j * C + cc] = a.P[(int64_t)j * a.ldp + c0 + cc];
   }
   __syncthreads();
   mark(0);
@@ -229,16 +234,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_gk_resident(ResArgs a) {
     grid.sync();
   };
 
-  // z = A^T q_1; alpha_1 = ||z|| (bidiag.py:139-147)
-  gemv_t(Qs, nullptr, 0.0);
-  double nrm2 = cgs2(Ps, C, 0, zv, nc);
+  // z = A^T q_{l+1}; alpha_{l+1} = ||z|| after CGS2 against the l kept
+  // right vectors (l = 0: the first product, bidiag.py:139-147; l > 0: the
+  // resumed loop of ksvd_run_restart)
+  const int l = a.l;
+  gemv_t(Qs + (size_t)l * R, nullptr, 0.0);
+  double nrm2 = cgs2(Ps, C, l, zv, nc);
   double alpha = sqrt(nrm2);
-  if (!isfinite(alpha)) return finish(ST_NONFINITE, 0);
-  if (alpha < a.eps) return finish(ST_DEGENERATE, 0);
-  if (b == 0 && tid == 0) a.alpha[1] = alpha;
-  publish_p(0, alpha);
+  if (!isfinite(alpha)) return finish(ST_NONFINITE, l);
+  if (alpha < a.eps) return finish(l == 0 ? ST_DEGENERATE : ST_ALPHA_BREAK, l);
+  if (b == 0 && tid == 0) a.alpha[l + 1] = alpha;
+  publish_p(l, alpha);
 
-  for (int i = 1; i <= a.k_max; ++i) {
+  for (int i = l + 1; i <= a.k_max; ++i) {
     // w = A p_i - alpha_i q_i (bidiag.py:152); p staged in shared memory
     bulk(pv, a.pvec, (uint32_t)(((n + 1) & ~(int64_t)1) * sizeof(double)));
     for (int r = warp; r < nr; r += kWarps) {
@@ -438,6 +446,113 @@ k_multi_rhs_rows(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t n,
       if (lane == 0) Y[(int64_t)t * ldy + r] = sigma ? v / sigma[t] : v;
     }
   }
+}
+
+}  // namespace ksvd
+
+namespace ksvd {
+
+// Dense SVD T = U diag(s) V^T of the restarted mode's small projected
+// matrix in ONE CTA (north star (d): "the tiny SVD on the host or in a
+// single-CTA kernel"): one-sided Jacobi with the round-robin (circle)
+// ordering, so the k/2 column pairs of a round rotate in parallel, one warp
+// per pair.  W = T and V live in shared memory; converged when a whole
+// sweep made no rotation (|g| <= k eps sqrt(a b), columns below eps ||T||_F
+// count as zero -- the host ksvd_dense_svd rule).  Output sorted descending,
+// U[:, j] = W[:, j] / s_j (0 for s_j = 0).  Fixed order: deterministic.
+constexpr int kSvdThreads = 1024, kSvdWarps = kSvdThreads / 32;
+__global__ void __launch_bounds__(kSvdThreads, 1)
+k_dense_svd_cta(int k, const double* __restrict__ T, double* __restrict__ U,
+                double* __restrict__ s, double* __restrict__ V, int* __restrict__ info) {
+  extern __shared__ __align__(16) double sv_smem[];
+  const int kk = (k + 1) & ~1;  // even number of players (a dummy when k is odd)
+  double* W = sv_smem;                 // kk x k, column-major (ld = k)
+  double* Vm = W + (size_t)kk * k;     // kk x k
+  double* nrm = Vm + (size_t)kk * k;   // kk
+  __shared__ int rotated;
+  __shared__ double fro2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < kk * k; e += kSvdThreads) {
+    const int j = e / k, i = e - j * k;
+    W[e] = j < k ? T[(size_t)j * k + i] : 0.0;
+    Vm[e] = (j < k && i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    double t = 0.0;
+    for (int e = lane; e < k * k; e += 32) t = fma(W[e], W[e], t);
+    t = warp_sum(t);
+    if (lane == 0) fro2 = t;
+  }
+  __syncthreads();
+  const double tol = fmax(1e-15, (double)k * DBL_EPSILON);
+  const double zero2 = fro2 * DBL_EPSILON * DBL_EPSILON;
+  int sweep = 0;
+  for (; sweep < 80; ++sweep) {
+    if (tid == 0) rotated = 0;
+    __syncthreads();
+    for (int r = 0; r < kk - 1; ++r) {
+      for (int slot = warp; slot < kk / 2; slot += kSvdWarps) {
+        auto elem = [&](int j) { return j == 0 ? 0 : 1 + (j - 1 + r) % (kk - 1); };
+        int p = elem(slot), q = elem(kk - 1 - slot);
+        if (p > q) {
+          const int x = p;
+          p = q;
+          q = x;
+        }
+        if (q >= k) continue;  // the dummy player
+        double* wp = W + (size_t)p * k;
+        double* wq = W + (size_t)q * k;
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (int i = lane; i < k; i += 32) {
+          a = fma(wp[i], wp[i], a);
+          b = fma(wq[i], wq[i], b);
+          g = fma(wp[i], wq[i], g);
+        }
+        a = warp_sum(a);
+        b = warp_sum(b);
+        g = warp_sum(g);
+        if (g == 0.0 || a <= zero2 || b <= zero2 || fabs(g) <= tol * sqrt(a * b)) continue;
+        if (lane == 0) rotated = 1;
+        const double zeta = (b - a) / (2.0 * g);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
+        double* vp = Vm + (size_t)p * k;
+        double* vq = Vm + (size_t)q * k;
+        for (int i = lane; i < k; i += 32) {
+          const double x = wp[i], y = wq[i];
+          wp[i] = c * x - sn * y;
+          wq[i] = sn * x + c * y;
+          const double u = vp[i], v = vq[i];
+          vp[i] = c * u - sn * v;
+          vq[i] = sn * u + c * v;
+        }
+      }
+      __syncthreads();
+    }
+    const bool any = rotated != 0;
+    __syncthreads();
+    if (!any) break;
+  }
+  for (int j = warp; j < k; j += kSvdWarps) {
+    double t = 0.0;
+    for (int i = lane; i < k; i += 32) t = fma(W[(size_t)j * k + i], W[(size_t)j * k + i], t);
+    t = warp_sum(t);
+    if (lane == 0) nrm[j] = sqrt(t);
+  }
+  __syncthreads();
+  // descending order, ties by index (the host rule); k <= ~110: rank by count
+  for (int j = tid; j < k; j += kSvdThreads) {
+    int rank = 0;
+    for (int o = 0; o < k; ++o)
+      if (nrm[o] > nrm[j] || (nrm[o] == nrm[j] && o < j)) ++rank;
+    s[rank] = nrm[j];
+    for (int i = 0; i < k; ++i) {
+      U[(size_t)rank * k + i] = nrm[j] > 0 ? W[(size_t)j * k + i] / nrm[j] : 0.0;
+      V[(size_t)rank * k + i] = Vm[(size_t)j * k + i];
+    }
+  }
+  if (tid == 0) *info = sweep;
 }
 
 }  // namespace ksvd

@@ -45,13 +45,21 @@ class RestartInfo:
     k_prime: int             # size of the final projected matrix
 
 
-def dense_svd(T: np.ndarray):
-    """(Uh, s, Vh) of a small square matrix on the host (native Jacobi)."""
+def dense_svd(T: np.ndarray, ctx: _lib.Context | None = None):
+    """(Uh, s, Vh) of a small square matrix: host Jacobi (ksvd_dense_svd), or
+    the one-CTA device kernel when a context is given (ksvd_dense_svd_dev;
+    measured slower at these sizes -- 29 latency-bound rounds per sweep --
+    so fsvd_restarted uses the host routine)."""
     k = T.shape[0]
     Tc = _colmajor(T)
     Ut, Vt, s = np.empty((k, k)), np.empty((k, k)), np.empty(k)
-    _lib.check(_lib.load_library().ksvd_dense_svd(k, _lib.dptr(Tc), _lib.dptr(Ut), _lib.dptr(s),
-                                                  _lib.dptr(Vt)))
+    lib = _lib.load_library()
+    if ctx is not None:
+        _lib.check(lib.ksvd_dense_svd_dev(ctx.handle, k, _lib.dptr(Tc), _lib.dptr(Ut),
+                                          _lib.dptr(s), _lib.dptr(Vt)))
+    else:
+        _lib.check(lib.ksvd_dense_svd(k, _lib.dptr(Tc), _lib.dptr(Ut), _lib.dptr(s),
+                                      _lib.dptr(Vt)))
     return Ut.T, s, Vt.T
 
 
@@ -125,7 +133,7 @@ def fsvd_restarted(A, r: int, k: int | None = None, tol: float = 1e-10,
         head, restarts, steps = None, 0, kp
         while True:
             T, kq, kpc = _projected(a, b, kp, flags, head)
-            Uh, s, Vh = dense_svd(T)
+            Uh, s, Vh = dense_svd(T)  # host Jacobi: faster than the 1-CTA kernel at k <= 100
             early = bool(flags & _lib.RUN_EARLY)
             resid = np.zeros(T.shape[0]) if early else abs(b[kp]) * np.abs(Uh[kp - 1, :])
             s1 = float(s[0]) if s.size else 0.0

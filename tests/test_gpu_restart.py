@@ -110,3 +110,23 @@ def test_restarted_multi_rank_code_path():
     assert res.returncode == 0, res.stderr[-2000:]
     err, restarts, conv = json.loads(res.stdout.strip().splitlines()[-1])
     assert err <= 1e-10 and restarts >= 1 and conv
+
+
+def test_dense_svd_single_cta_kernel():
+    """k_dense_svd_cta (ksvd_dense_svd_dev) against LAPACK, incl. odd k (the
+    dummy round-robin player), exact zero singular values and the host
+    fallback above the shared-memory limit."""
+    from paper_2104_10785_b200 import _lib
+    from paper_2104_10785_b200.restart import dense_svd
+    ctx = _lib.get_context()
+    rng = np.random.default_rng(11)
+    for k in (1, 2, 7, 30, 31, 64, 101, 130):
+        T = np.triu(rng.standard_normal((k, k)))
+        if k > 5:
+            T[-1, :] = 0.0  # a zero singular value (an alpha breakdown's T)
+        Uh, s, Vh = dense_svd(T, ctx)
+        ref = np.linalg.svd(T, compute_uv=False)
+        assert np.allclose(s, ref, rtol=1e-12, atol=1e-14 * ref[0]), k
+        assert np.allclose((Uh * s) @ Vh.T, T, atol=1e-12 * ref[0]), k
+        assert np.allclose(Vh.T @ Vh, np.eye(k), atol=1e-12), k
+        assert np.all(np.diff(s) <= 0)
