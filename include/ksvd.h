@@ -66,6 +66,7 @@ extern "C" {
 #define KSVD_RUN_ALPHA_BREAK 8 /* alpha_{k'+1} < eps (bidiag.py:174-176)       */
 
 #define KSVD_NCCL_UID_BYTES 128
+#define KSVD_PX_HANDLE_BYTES 64
 
 typedef struct ksvd_ctx ksvd_ctx;
 typedef struct ksvd_mat ksvd_mat;
@@ -95,6 +96,17 @@ int ksvd_ctx_launch_count(ksvd_ctx *ctx, int64_t *launches);
 /* Device time (ms) between two context-stream marks; used by bench. */
 int ksvd_ctx_mark(ksvd_ctx *ctx, int slot);
 int ksvd_ctx_elapsed(ksvd_ctx *ctx, int slot0, int slot1, float *ms);
+/* NVLink peer exchange (multi-rank; replaces ncclAllReduce for the GK
+ * step's vectors up to `slot` doubles, reference counterpart: none -- the
+ * reference is single-process).  Collective, in two halves around the
+ * host-side all-gather of the handles: ksvd_px_export allocates this
+ * rank's receive area and writes its CUDA IPC handle (KSVD_PX_HANDLE_BYTES);
+ * ksvd_px_open maps every peer's area (handles: nranks x 64 bytes in rank
+ * order), self-tests against NCCL and enables the exchange only if every
+ * rank agrees (ksvd_px_enabled reports the outcome). */
+int ksvd_px_export(ksvd_ctx *ctx, int64_t slot, unsigned char *handle);
+int ksvd_px_open(ksvd_ctx *ctx, const unsigned char *handles);
+int ksvd_px_enabled(ksvd_ctx *ctx, int *on);
 
 /* ---- matrices ----------------------------------------------------------
  * rows: host pointer to the m_local local rows (row-major, src_ld elements

@@ -22,6 +22,7 @@ LIB_PATH = _HERE / "libksvd.so"
 
 KSVD_OK, KSVD_ERUNTIME, KSVD_ECONFIG, KSVD_ENUMERIC = 0, 1, 2, 3
 KSVD_F64, KSVD_F32 = 0, 1
+PX_HANDLE_BYTES = 64
 RUN_EARLY, RUN_DEGENERATE, RUN_BETA_BREAK, RUN_ALPHA_BREAK = 1, 2, 4, 8
 NCCL_UID_BYTES = 128
 
@@ -80,6 +81,9 @@ SIGNATURES = {
     "ksvd_matrix_to_klrm": (C.c_int, [_vp, C.c_char_p]),
     "ksvd_dense_svd": (C.c_int, [C.c_int, _pd, _pd, _pd, _pd]),
     "ksvd_dense_svd_dev": (C.c_int, [_vp, C.c_int, _pd, _pd, _pd, _pd]),
+    "ksvd_px_export": (C.c_int, [_vp, C.c_int64, C.c_char_p]),
+    "ksvd_px_open": (C.c_int, [_vp, C.c_char_p]),
+    "ksvd_px_enabled": (C.c_int, [_vp, _pi]),
     "ksvd_run_restart": (C.c_int, [_vp, C.c_int, _pd, _pd, C.c_int]),
     "ksvd_run_ritz_bases": (C.c_int, [_vp, _pd, C.c_int, _pd, C.c_int, C.c_int, _pd, _pd]),
     "ksvd_matrix_from_factors": (C.c_int, [_vp, _pd, _pd, _pd, C.c_int64, C.c_int64, C.c_int64,
@@ -171,6 +175,21 @@ class Context:
         ms = C.c_float()
         check(load_library().ksvd_ctx_elapsed(self.handle, s0, s1, C.byref(ms)))
         return float(ms.value)
+
+    # ---- NVLink peer exchange (dist.init_distributed(peer_exchange=True)) ----
+    def px_export(self, slot: int) -> bytes:
+        buf = C.create_string_buffer(PX_HANDLE_BYTES)
+        check(load_library().ksvd_px_export(self.handle, int(slot), buf))
+        return buf.raw
+
+    def px_open(self, handles: bytes) -> bool:
+        check(load_library().ksvd_px_open(self.handle, handles))
+        return self.px_enabled()
+
+    def px_enabled(self) -> bool:
+        on = C.c_int()
+        check(load_library().ksvd_px_enabled(self.handle, C.byref(on)))
+        return bool(on.value)
 
 
 _ctx: Context | None = None

@@ -29,6 +29,7 @@
 #include "kernels.cuh"
 #include "klrm.cuh"
 #include "resident.cuh"
+#include "peer.cuh"
 #include "ksvd.h"
 
 using namespace ksvd;
@@ -82,6 +83,16 @@ struct ksvd_ctx {
   int device = 0, rank = 0, nranks = 1, sms = 148;
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
+  // NVLink peer exchange (peer.cuh): replaces ncclAllReduce once opened
+  bool px = false;
+  int64_t px_slot = 0;
+  void* px_local = nullptr;  // this rank's receive area + counters (IPC-exported)
+  double* px_recv[kPxMaxRanks] = {};
+  unsigned long long* px_cnt[kPxMaxRanks] = {};
+  void* px_mapped[kPxMaxRanks] = {};  // opened IPC mappings (to close)
+  unsigned long long px_seq = 0;
+  unsigned long long px_arrivals = 0;  // cumulative CTAs each sender has pushed (same on all ranks)
+  int* px_err = nullptr;
   int64_t launches = 0;
   bool profiling = false;
   struct Prof {
@@ -183,8 +194,36 @@ static int launch_step(ksvd_ctx* c, int cls, void (*kernel)(KArgs...), dim3 grid
   return launch_impl(c, cls, pdl_enabled(c), kernel, grid, block, smem, args...);
 }
 
+static int px_allreduce(ksvd_ctx* c, double* buf, size_t count) {
+  PxArgs a{};
+  a.buf = buf;
+  a.L = (int64_t)count;
+  for (int r = 0; r < c->nranks; ++r) {
+    a.recv[r] = c->px_recv[r];
+    a.cnt[r] = c->px_cnt[r];
+  }
+  a.my_recv = c->px_recv[c->rank];
+  a.my_cnt = c->px_cnt[c->rank];
+  a.rank = c->rank;
+  a.N = c->nranks;
+  a.seq = ++c->px_seq;
+  a.slot = c->px_slot;
+  a.err = c->px_err;
+  // a few CTAs: every CTA spins until all peers' CTAs have pushed, so the
+  // grid stays far below one wave
+  const int64_t G = std::max<int64_t>(1, std::min<int64_t>(16, cdiv((int64_t)count, 2048)));
+  c->px_arrivals += (unsigned long long)G;  // counters are cumulative over collectives
+  a.want = c->px_arrivals;
+  k_px_allreduce<<<(unsigned)G, kThreads, 0, c->stream>>>(a);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(KSVD_ERUNTIME, "peer all-reduce: %s", cudaGetErrorString(e));
+  c->launches++;
+  return 0;
+}
+
 static int allreduce(ksvd_ctx* c, double* buf, size_t count) {
   if (!c->comm || count == 0) return 0;
+  if (c->px && (int64_t)count <= c->px_slot) return px_allreduce(c, buf, count);
   NK(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, c->comm, c->stream));
   return 0;
 }
@@ -899,6 +938,11 @@ static int read_state(ksvd_run* R) {
   DevState h{};
   CK(cudaMemcpyAsync(&h, R->st, sizeof h, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  if (c->px) {
+    int err = 0;
+    CK(cudaMemcpy(&err, c->px_err, sizeof err, cudaMemcpyDeviceToHost));
+    if (err) return set_err(KSVD_ERUNTIME, "peer exchange: a peer never arrived (timeout)");
+  }
   R->status = h.status;
   R->flags = 0;
   switch (h.status) {
@@ -1581,12 +1625,17 @@ int ksvd_ctx_create(int device, int rank, int nranks, const char* uid, ksvd_ctx*
     ncclUniqueId id;
     memcpy(&id, uid, sizeof id);
     NK(ncclCommInitRank(&c->comm, nranks, id, rank));
-  } else if (getenv("KSVD_FORCE_NCCL")) {
+  } else if (getenv("KSVD_FORCE_NCCL") || getenv("KSVD_FORCE_PX")) {
     // test hook: a 1-rank communicator exercises the multi-rank code path
     // (all-reduces between the kernels) on a single GPU
     ncclUniqueId id;
     NK(ncclGetUniqueId(&id));
     NK(ncclCommInitRank(&c->comm, 1, id, 0));
+    if (getenv("KSVD_FORCE_PX")) {  // ... and the peer exchange over a 1-rank group
+      unsigned char h[KSVD_PX_HANDLE_BYTES];
+      TRY(ksvd_px_export(c, 1 << 17, h));
+      TRY(ksvd_px_open(c, h));
+    }
   }
   *out = c;
   return 0;
@@ -1596,6 +1645,10 @@ int ksvd_ctx_destroy(ksvd_ctx* c) {
   if (!c) return 0;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  for (int r = 0; r < kPxMaxRanks; ++r)
+    if (c->px_mapped[r]) cudaIpcCloseMemHandle(c->px_mapped[r]);
+  if (c->px_local) cudaFree(c->px_local);
+  if (c->px_err) cudaFree(c->px_err);
   if (c->comm) ncclCommDestroy(c->comm);
   for (auto& p : c->pending) {
     cudaEventDestroy(p.a);
@@ -1607,6 +1660,83 @@ int ksvd_ctx_destroy(ksvd_ctx* c) {
   if (c->hprog) cudaFreeHost(c->hprog);
   cudaStreamDestroy(c->stream);
   delete c;
+  return 0;
+}
+
+int ksvd_px_export(ksvd_ctx* c, int64_t slot, unsigned char* handle) {
+  if (!c->comm) return set_err(KSVD_ECONFIG, "peer exchange needs a multi-rank context");
+  if (c->nranks > kPxMaxRanks)
+    return set_err(KSVD_ECONFIG, "peer exchange supports up to %d ranks", kPxMaxRanks);
+  if (slot < 1 || c->px_local) return set_err(KSVD_ECONFIG, "peer exchange: slot %lld",
+                                              (long long)slot);
+  CK(cudaSetDevice(c->device));
+  const size_t recv = sizeof(double) * 2 * (size_t)c->nranks * slot;
+  const size_t bytes = recv + sizeof(unsigned long long) * kPxCntStride * c->nranks;
+  CK(cudaMalloc(&c->px_local, bytes));  // IPC needs a plain cudaMalloc allocation
+  CK(cudaMemset(c->px_local, 0, bytes));
+  CK(cudaMalloc((void**)&c->px_err, sizeof(int)));
+  CK(cudaMemset(c->px_err, 0, sizeof(int)));
+  c->px_slot = slot;
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, c->px_local));
+  static_assert(sizeof(h) == KSVD_PX_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle, &h, sizeof h);
+  return 0;
+}
+
+int ksvd_px_open(ksvd_ctx* c, const unsigned char* handles) {
+  if (!c->px_local) return set_err(KSVD_ECONFIG, "ksvd_px_export first");
+  CK(cudaSetDevice(c->device));
+  const size_t recv = sizeof(double) * 2 * (size_t)c->nranks * c->px_slot;
+  for (int r = 0; r < c->nranks; ++r) {
+    char* base;
+    if (r == c->rank) {
+      base = static_cast<char*>(c->px_local);
+    } else {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, handles + (size_t)r * KSVD_PX_HANDLE_BYTES, sizeof h);
+      void* p = nullptr;
+      CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      c->px_mapped[r] = p;
+      base = static_cast<char*>(p);
+    }
+    c->px_recv[r] = reinterpret_cast<double*>(base);
+    c->px_cnt[r] = reinterpret_cast<unsigned long long*>(base + recv);
+  }
+  // self-test against NCCL on every rank; enabled only if it agrees everywhere
+  const int64_t L = std::min<int64_t>(c->px_slot, 4099);
+  double* v = nullptr;
+  CK(cudaMalloc(&v, sizeof(double) * 2 * L + sizeof(double)));
+  std::vector<double> h0(L), h1(L);
+  for (int64_t i = 0; i < L; ++i) h0[i] = (double)((c->rank + 1) * (i % 97) + 0.25 * i);
+  CK(cudaMemcpy(v, h0.data(), sizeof(double) * L, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(v + L, h0.data(), sizeof(double) * L, cudaMemcpyHostToDevice));
+  int rc = px_allreduce(c, v, (size_t)L);
+  if (!rc) {
+    ncclResult_t nr = ncclAllReduce(v + L, v + L, L, ncclDouble, ncclSum, c->comm, c->stream);
+    if (nr != ncclSuccess) rc = set_err(KSVD_ERUNTIME, "nccl: %s", ncclGetErrorString(nr));
+  }
+  int err = 0;
+  if (!rc) {
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpy(h0.data(), v, sizeof(double) * L, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(h1.data(), v + L, sizeof(double) * L, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&err, c->px_err, sizeof(int), cudaMemcpyDeviceToHost));
+  }
+  // exact agreement is expected: small integers and quarters sum exactly
+  double ok = (!rc && !err && h0 == h1) ? 1.0 : 0.0;
+  CK(cudaMemcpy(v, &ok, sizeof(double), cudaMemcpyHostToDevice));
+  NK(ncclAllReduce(v, v, 1, ncclDouble, ncclSum, c->comm, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(&ok, v, sizeof(double), cudaMemcpyDeviceToHost));
+  cudaFree(v);
+  c->px = ok == (double)c->nranks;
+  if (!c->px) fprintf(stderr, "[ksvd] peer exchange self-test failed on some rank: using NCCL\n");
+  return rc;
+}
+
+int ksvd_px_enabled(ksvd_ctx* c, int* on) {
+  *on = c->px ? 1 : 0;
   return 0;
 }
 

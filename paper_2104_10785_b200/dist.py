@@ -28,10 +28,31 @@ def broadcast_uid(uid: bytes | None, rank: int) -> bytes:
     return bytes(out)
 
 
-def init_distributed(device: int | None = None) -> _lib.Context:
+PX_SLOT = 1 << 17  # doubles per sender slot of the peer exchange (1 MB)
+
+
+def open_peer_exchange(ctx: _lib.Context, slot: int = PX_SLOT) -> bool:
+    """Map every rank's receive area over CUDA IPC (handles all-gathered over
+    torch.distributed) so the GK step's all-reduces run as one NVLink kernel
+    (csrc/peer.cuh) instead of ncclAllReduce.  Collective; returns whether
+    the exchange passed its self-test on every rank (NCCL stays otherwise)."""
+    import torch.distributed as dist
+
+    mine = ctx.px_export(slot)
+    allh = [None] * ctx.nranks
+    dist.all_gather_object(allh, mine)
+    if any(not isinstance(h, (bytes, bytearray)) or len(h) != _lib.PX_HANDLE_BYTES
+           for h in allh):
+        raise RuntimeError("bad peer-exchange handle all-gather")
+    return ctx.px_open(b"".join(bytes(h) for h in allh))
+
+
+def init_distributed(device: int | None = None,
+                     peer_exchange: bool | None = None) -> _lib.Context:
     """Create this rank's context (NCCL communicator when world > 1) and make
     it the process default.  Requires torch.distributed to be initialised
-    when WORLD_SIZE > 1."""
+    when WORLD_SIZE > 1.  peer_exchange (default: env KSVD_P2P=1) maps the
+    NVLink peer exchange for the step all-reduces."""
     import torch.distributed as dist
 
     if dist.is_available() and dist.is_initialized():
@@ -48,4 +69,8 @@ def init_distributed(device: int | None = None) -> _lib.Context:
         uid = broadcast_uid(_lib.nccl_unique_id() if rank == 0 else None, rank)
     ctx = _lib.Context(device=device, rank=rank, nranks=world, uid=uid)
     _lib.set_context(ctx)
+    if peer_exchange is None:
+        peer_exchange = os.environ.get("KSVD_P2P") == "1"
+    if world > 1 and peer_exchange:
+        open_peer_exchange(ctx)
     return ctx

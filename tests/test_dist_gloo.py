@@ -1,6 +1,8 @@
 """Multi-rank host logic on CPU: world_size 2 over gloo.
 
 * the NCCL unique-id broadcast used by dist.init_distributed();
+* the all-gather of the NVLink peer-exchange IPC handles
+  (dist.open_peer_exchange);
 * the row-sharded GK arithmetic (tests/sharded_model.py, the same data
   movement as the CUDA path at N GPUs) against the single-process oracle:
   alphas/betas, k', the gathered left basis and the rank count.
@@ -40,6 +42,27 @@ def _worker(rank, world, port, q):
         uid = _lib.nccl_unique_id() if rank == 0 else None
         got = broadcast_uid(uid, rank)
         out["uid"] = got
+
+        # peer-exchange plumbing: every rank's IPC handle reaches every rank
+        # in rank order (the context is mocked: no GPU here)
+        from paper_2104_10785_b200.dist import open_peer_exchange
+
+        class _MockCtx:
+            nranks = world
+
+            def __init__(self):
+                self.rank, self.slot, self.handles = rank, None, None
+
+            def px_export(self, slot):
+                self.slot = slot
+                return bytes([17 * (rank + 1)]) * _lib.PX_HANDLE_BYTES
+
+            def px_open(self, handles):
+                self.handles = handles
+                return True
+
+        mctx = _MockCtx()
+        out["px"] = (open_peer_exchange(mctx, slot=4096), mctx.slot, mctx.handles)
         cases = [(301, 120, 25, 60, 3), (1000, 400, 100, 400, 5), (257, 200, 200, 200, 11)]
         res = []
         for m, n, l, k, seed in cases:
@@ -73,6 +96,10 @@ def test_two_rank_sharded_gk_matches_oracle():
         assert p.exitcode == 0
     # every rank received rank 0's NCCL id
     assert outs[0]["uid"] == outs[1]["uid"] and len(outs[0]["uid"]) == 128
+    # ... and every rank's peer-exchange handle, in rank order
+    want = b"".join(bytes([17 * (r + 1)]) * 64 for r in range(world))
+    for r in range(world):
+        assert outs[r]["px"] == (True, 4096, want)
     cases = [(301, 120, 25, 60, 3), (1000, 400, 100, 400, 5), (257, 200, 200, 200, 11)]
     for ci, (m, n, l, k, seed) in enumerate(cases):
         A = low_rank_synth(m, n, l, seed=seed)

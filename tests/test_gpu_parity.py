@@ -281,7 +281,7 @@ _MULTI = {"KSVD_RESIDENT": "0"}  # small cases would otherwise take the resident
 
 
 @pytest.mark.parametrize("env", [{"KSVD_TILE": "0", **_MULTI}, {"KSVD_COOP": "0", **_MULTI},
-                                 {"KSVD_FORCE_NCCL": "1"},
+                                 {"KSVD_FORCE_NCCL": "1"}, {"KSVD_FORCE_PX": "1"},
                                  {"KSVD_COOP_GLOBAL": "1", "KSVD_TILE": "0", **_MULTI},
                                  {"KSVD_CGS_SYNC": "5", **_MULTI}, {"KSVD_RED_MAX": "0", **_MULTI},
                                  {"KSVD_RED_MAX": "100000000", **_MULTI}, {"KSVD_PDL": "0", **_MULTI},
@@ -292,7 +292,8 @@ def test_cgs_paths_agree(env):
     multi-kernel CGS2 paths (selected at load time) all meet the parity bar,
     with and without programmatic dependent launch; KSVD_FORCE_NCCL runs the
     multi-rank code path (NCCL all-reduces between the kernels) over a
-    1-rank communicator."""
+    1-rank communicator, KSVD_FORCE_PX the same path with every all-reduce
+    through the NVLink peer-exchange kernel (csrc/peer.cuh) instead."""
     import json
     import os
     import subprocess
