@@ -194,7 +194,7 @@ static int launch_step(ksvd_ctx* c, int cls, void (*kernel)(KArgs...), dim3 grid
   return launch_impl(c, cls, pdl_enabled(c), kernel, grid, block, smem, args...);
 }
 
-static int px_allreduce(ksvd_ctx* c, double* buf, size_t count) {
+static PxArgs px_args(ksvd_ctx* c, double* buf, size_t count, int64_t* grid) {
   PxArgs a{};
   a.buf = buf;
   a.L = (int64_t)count;
@@ -209,11 +209,17 @@ static int px_allreduce(ksvd_ctx* c, double* buf, size_t count) {
   a.seq = ++c->px_seq;
   a.slot = c->px_slot;
   a.err = c->px_err;
-  // a few CTAs: every CTA spins until all peers' CTAs have pushed, so the
-  // grid stays far below one wave
+  // a few CTAs (each spins until all peers' CTAs pushed: far below a wave)
   const int64_t G = std::max<int64_t>(1, std::min<int64_t>(16, cdiv((int64_t)count, 2048)));
   c->px_arrivals += (unsigned long long)G;  // counters are cumulative over collectives
   a.want = c->px_arrivals;
+  *grid = G;
+  return a;
+}
+
+static int px_allreduce(ksvd_ctx* c, double* buf, size_t count) {
+  int64_t G = 1;
+  const PxArgs a = px_args(c, buf, count, &G);
   k_px_allreduce<<<(unsigned)G, kThreads, 0, c->stream>>>(a);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(KSVD_ERUNTIME, "peer all-reduce: %s", cudaGetErrorString(e));
@@ -444,6 +450,19 @@ static int dense_gemv_t(ksvd_mat* M, const double* q_src, const double* q_scale,
   const int nsplit = M->mloc > 0 ? (int)pt.nsplit : 1;
   const bool multi = c->comm != nullptr;
   if (!finalize && !multi) return 0;  // fused into the caller's k_cgs2_coop
+  if (multi && c->px && M->n_pad <= c->px_slot) {
+    // split sums + peer exchange + (- beta p) + check in one kernel
+    int64_t G = 1;
+    const PxArgs a = px_args(c, z, (size_t)M->n_pad, &G);
+    k_gemv_t_fin_px<<<(unsigned)G, kThreads, 0, c->stream>>>(
+        a, (const double*)M->part_t, M->n_pad, nsplit, M->n, beta, pprev, st, step,
+        (int)check);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+      return set_err(KSVD_ERUNTIME, "A^T q exchange: %s", cudaGetErrorString(e));
+    c->launches++;
+    return 0;
+  }
   TRY(launch(c, KC_FIN, k_gemv_t_finalize, dim3((unsigned)cdiv(M->n_pad, 32)),
              dim3(kThreads), 0, (const double*)M->part_t, M->n_pad, nsplit, M->n,
              M->n_pad, multi ? (const double*)nullptr : beta,

@@ -78,4 +78,50 @@ __global__ void __launch_bounds__(kThreads) k_px_allreduce(PxArgs a) {
   }
 }
 
+// The multi-rank A^T q epilogue as ONE kernel: the split partial sums of
+// k_gemv_t2 reduced for this CTA's columns (fixed order), pushed straight
+// into every peer's slot, the cross-rank sum in rank order, then
+// z -= beta p and the non-finite check (k_gemv_t_finalize + all-reduce +
+// k_axpy_check fused).  Never skips on a halted run: every rank pushes and
+// counts in every call, so the cumulative counters stay in step.
+__global__ void __launch_bounds__(kThreads)
+k_gemv_t_fin_px(PxArgs a, const double* __restrict__ part, int64_t ldz, int nsplit, int64_t n,
+                const double* __restrict__ beta, const double* __restrict__ pprev,
+                DevState* st, int step, int check) {
+  const int par = (int)(a.seq & 1);
+  const int64_t chunk = (a.L + gridDim.x - 1) / gridDim.x;
+  const int64_t e0 = (int64_t)blockIdx.x * chunk;
+  const int64_t e1 = min(a.L, e0 + chunk);
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += kThreads) {
+    double v = 0.0;
+    if (e < n)
+      for (int k = 0; k < nsplit; ++k) v += part[(int64_t)k * ldz + e];
+    for (int r = 0; r < a.N; ++r) a.recv[r][((int64_t)par * a.N + a.rank) * a.slot + e] = v;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x < a.N)
+    atomicAdd_system(a.cnt[threadIdx.x] + (int64_t)a.rank * kPxCntStride, 1ull);
+  if (threadIdx.x < a.N) {
+    const unsigned long long* c = a.my_cnt + (int64_t)threadIdx.x * kPxCntStride;
+    long long spins = 0;
+    while (ld_acquire_sys(c) < a.want) {
+      if (*reinterpret_cast<volatile int*>(a.err) || ++spins > (1ll << 23)) {
+        atomicExch(a.err, 1);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  __threadfence_system();
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += kThreads) {
+    double v = 0.0;
+    for (int s = 0; s < a.N; ++s) v += __ldcg(a.my_recv + ((int64_t)par * a.N + s) * a.slot + e);
+    if (e < n && pprev) v = v - (*beta) * pprev[e];
+    a.buf[e] = e < n ? v : 0.0;
+    if (check && e < n) flag_nonfinite(st, v, step);
+  }
+}
+
 }  // namespace ksvd
