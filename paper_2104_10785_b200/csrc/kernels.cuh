@@ -120,20 +120,20 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 
-// sum_{k < cnt} p[k*ld] with 8 loads in flight and 4 interleaved partial
-// sums combined in a fixed order (deterministic; not latency-chained)
+// sum_{k < cnt} p[k*ld] with up to 16 loads in flight (predicated, so a
+// whole batch is one L2 round trip) and 4 interleaved partial sums combined
+// in a fixed order (deterministic; not latency-chained).  The finalisation
+// of k_gemv_n2's 20 chunk partials (config 2) is 2 round trips, not 3.
 __device__ __forceinline__ double strided_sum(const double* __restrict__ p, int64_t ld,
                                               int cnt) {
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  int k = 0;
-  for (; k + 8 <= cnt; k += 8) {
-    double t[8];
+  for (int k = 0; k < cnt; k += 16) {
+    double t[16];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) t[u] = p[(int64_t)(k + u) * ld];
+    for (int u = 0; u < 16; ++u) t[u] = k + u < cnt ? p[(int64_t)(k + u) * ld] : 0.0;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc[u & 3] += t[u];
+    for (int u = 0; u < 16; ++u) acc[u & 3] += t[u];
   }
-  for (; k < cnt; ++k) acc[k & 3] += p[(int64_t)k * ld];
   return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
