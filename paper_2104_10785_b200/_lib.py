@@ -100,7 +100,8 @@ def load_library(path: Path | str | None = None) -> C.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        # KSVD_LIB_PATH: load another build of the library (A/B measurements)
+        p = Path(path) if path else Path(os.environ.get("KSVD_LIB_PATH", LIB_PATH))
         if not p.exists():
             raise RuntimeError(
                 f"{p} is missing: build it with `python -m paper_2104_10785_b200.build` "

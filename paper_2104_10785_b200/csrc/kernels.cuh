@@ -130,7 +130,7 @@ __device__ __forceinline__ double strided_sum(const double* __restrict__ p, int6
   for (int k = 0; k < cnt; k += 16) {
     double t[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) t[u] = k + u < cnt ? p[(int64_t)(k + u) * ld] : 0.0;
+    for (int u = 0; u < 16; ++u) t[u] = k + u < cnt ? __ldcg(p + (int64_t)(k + u) * ld) : 0.0;
 #pragma unroll
     for (int u = 0; u < 16; ++u) acc[u & 3] += t[u];
   }
@@ -181,24 +181,35 @@ __device__ __forceinline__ void flag_nonfinite(DevState* st, double v, int step)
 // of the same rows, so a CTA reads long contiguous row segments.  Partials
 // per (chunk, row) go to part[chunk*m + row]; k_gemv_n_finalize adds them
 // in chunk order and applies - alpha q.
-template <typename TA, int U, int RB = 8, int PF = 0>
-__global__ void __launch_bounds__(kThreads)
-k_gemv_n2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nchunks,
-          int64_t nseg, const double* __restrict__ p_src,
-          const double* __restrict__ p_scale, double* __restrict__ p_dst, int64_t n_true,
-          double* __restrict__ part, const DevState* st) {
+// Loads of vectors another CTA wrote: through L2 (ld.global.cg) inside a
+// persistent kernel (L1 is not coherent), plain cached loads otherwise --
+// measured: the L1 reuse of p / q across a standalone launch's CTAs is worth
+// 1-4 % of the A-streaming kernels.
+template <bool CG>
+__device__ __forceinline__ double ldv(const double* p) {
+  if constexpr (CG) return __ldcg(p);
+  else return *p;
+}
+
+// The body is a device function so the persistent streaming kernel
+// (stream.cuh) runs the same code with the same work decomposition; p, its
+// scale and the partials go through L2 (__ldcg): inside a persistent kernel
+// they were written by other CTAs of the same launch.
+template <typename TA, int U, int RB = 8, int PF = 0, bool CG = false>
+__device__ __forceinline__ void gemv_n2_body(const TA* __restrict__ A, int64_t lda, int64_t m,
+                                             int64_t nvec, int nchunks, int64_t nseg,
+                                             const double* __restrict__ p_src,
+                                             const double* __restrict__ p_scale,
+                                             double* __restrict__ p_dst, int64_t n_true,
+                                             double* __restrict__ part, int64_t gw) {
   static_assert(RB % 8 == 0, "rows per iteration: multiple of 8");
-  pdl_wait();
-  pdl_trigger(1);
-  if (halted(st)) return;
   constexpr int V = AVec<TA>::V;
   constexpr int CW = 32 * U;
   const int lane = threadIdx.x & 31;
-  const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const int chunk = (int)(gw % nchunks);
   const int64_t rseg = gw / nchunks;
   if (rseg >= nseg) return;
-  const double scale = p_scale ? *p_scale : 1.0;
+  const double scale = p_scale ? ldv<CG>(p_scale) : 1.0;
   double pv[U][V];
   bool live[U];
 #pragma unroll
@@ -208,7 +219,7 @@ k_gemv_n2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nc
 #pragma unroll
     for (int k = 0; k < V; ++k) {
       const int64_t col = vi * V + k;
-      double x = (live[u] && col < n_true) ? p_src[col] : 0.0;
+      double x = (live[u] && col < n_true) ? ldv<CG>(p_src + col) : 0.0;
       if (p_scale) {
         x = x / scale;
         if (rseg == 0 && p_dst && live[u] && col < n_true) p_dst[col] = x;
@@ -261,6 +272,19 @@ k_gemv_n2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nc
       if ((lane & 3) == 0 && row < r_end) part[(int64_t)chunk * m + row] = t;
     }
   }
+}
+
+template <typename TA, int U, int RB = 8, int PF = 0>
+__global__ void __launch_bounds__(kThreads)
+k_gemv_n2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nchunks,
+          int64_t nseg, const double* __restrict__ p_src,
+          const double* __restrict__ p_scale, double* __restrict__ p_dst, int64_t n_true,
+          double* __restrict__ part, const DevState* st) {
+  pdl_wait();
+  pdl_trigger(1);
+  if (halted(st)) return;
+  gemv_n2_body<TA, U, RB, PF>(A, lda, m, nvec, nchunks, nseg, p_src, p_scale, p_dst, n_true,
+                              part, (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5));
 }
 
 // ---------------------------------------------------------------------------
@@ -547,27 +571,35 @@ k_gemv_t(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
 // and visited bottom-up (block = RG*U*IT rows; CTA s takes blocks s,
 // s + nsplit, ... from the last one): the whole grid then sweeps A upwards as
 // one band, starting on the rows k_gemv_n2 (top-down band) left in L2.
+// Shared-memory needs of gemv_t2_body (q staging + group sums), so callers
+// can provide them (static in k_gemv_t2, part of the dynamic carve-out in
+// the persistent kernel).
 template <typename TA, int U, int RG, int IT>
-__global__ void __launch_bounds__(kThreads)
-k_gemv_t2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
-          int64_t /*unused*/, const double* __restrict__ q_src,
-          const double* __restrict__ q_scale, double* __restrict__ q_dst,
-          double* __restrict__ part, int64_t ldz, const DevState* st) {
-  pdl_wait();
-  pdl_trigger(1);
-  if (halted(st)) return;
+struct GemvT2Smem {
+  static constexpr int V = AVec<TA>::V;
+  static constexpr int TPG = kThreads / RG;
+  static constexpr int QS = RG * U * IT;
+  static constexpr int RED = RG > 1 ? RG * TPG * V : 1;
+};
+
+template <typename TA, int U, int RG, int IT, bool CG = false>
+__device__ __forceinline__ void gemv_t2_body(const TA* __restrict__ A, int64_t lda, int64_t m,
+                                             int64_t nvec, const double* __restrict__ q_src,
+                                             const double* __restrict__ q_scale,
+                                             double* __restrict__ q_dst,
+                                             double* __restrict__ part, int64_t ldz,
+                                             int64_t bx, int64_t sp, int64_t nsplit,
+                                             double* __restrict__ q_s,
+                                             double* __restrict__ red_flat) {
   constexpr int V = AVec<TA>::V;
   constexpr int TPG = kThreads / RG;
   constexpr int RBT = RG * U * IT;
   static_assert(RBT <= kQB, "row block exceeds the q staging buffer");
-  __shared__ double q_s[RBT];
-  __shared__ double red[RG > 1 ? RG : 1][RG > 1 ? TPG * V : 1];
   const int g = threadIdx.x / TPG, t = threadIdx.x % TPG;
-  const int64_t vcol = (int64_t)blockIdx.x * TPG + t;
+  const int64_t vcol = bx * TPG + t;
   const bool active = vcol < nvec;
-  const int64_t nsplit = gridDim.y, sp = blockIdx.y;
   const int64_t nblk = (m + RBT - 1) / RBT;
-  const double scale = q_scale ? *q_scale : 1.0;
+  const double scale = q_scale ? ldv<CG>(q_scale) : 1.0;
   double acc[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.0;
@@ -578,10 +610,10 @@ k_gemv_t2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
     const int nr = (int)min((int64_t)RBT, m - rb);
     __syncthreads();
     for (int e = threadIdx.x; e < nr; e += kThreads) {
-      double qv = q_src[rb + e];
+      double qv = ldv<CG>(q_src + rb + e);
       if (q_scale) {
         qv = qv / scale;
-        if (blockIdx.x == 0 && q_dst) q_dst[rb + e] = qv;
+        if (bx == 0 && q_dst) q_dst[rb + e] = qv;
       }
       q_s[e] = qv;
     }
@@ -610,23 +642,40 @@ k_gemv_t2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
   }
   if constexpr (RG > 1) {
 #pragma unroll
-    for (int k = 0; k < V; ++k) red[g][t * V + k] = acc[k];
+    for (int k = 0; k < V; ++k) red_flat[g * (TPG * V) + t * V + k] = acc[k];
     __syncthreads();
     if (g == 0 && active) {
 #pragma unroll
       for (int k = 0; k < V; ++k) {
-        double sum = red[0][t * V + k];
+        double sum = red_flat[t * V + k];
 #pragma unroll
-        for (int gg = 1; gg < RG; ++gg) sum += red[gg][t * V + k];
+        for (int gg = 1; gg < RG; ++gg) sum += red_flat[gg * (TPG * V) + t * V + k];
         acc[k] = sum;
       }
     }
+    if constexpr (CG) __syncthreads();  // red is reused by the next virtual block
   }
   if (g == 0 && active) {
-    double* dst = part + (int64_t)blockIdx.y * ldz + vcol * V;
+    double* dst = part + sp * ldz + vcol * V;
 #pragma unroll
     for (int k = 0; k < V; ++k) dst[k] = acc[k];
   }
+}
+
+template <typename TA, int U, int RG, int IT>
+__global__ void __launch_bounds__(kThreads)
+k_gemv_t2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
+          int64_t /*unused*/, const double* __restrict__ q_src,
+          const double* __restrict__ q_scale, double* __restrict__ q_dst,
+          double* __restrict__ part, int64_t ldz, const DevState* st) {
+  pdl_wait();
+  pdl_trigger(1);
+  if (halted(st)) return;
+  using SM = GemvT2Smem<TA, U, RG, IT>;
+  __shared__ double q_s[SM::QS];
+  __shared__ double red[SM::RED];
+  gemv_t2_body<TA, U, RG, IT>(A, lda, m, nvec, q_src, q_scale, q_dst, part, ldz, blockIdx.x,
+                              blockIdx.y, gridDim.y, q_s, red);
 }
 
 // z[j] = sum_s part[s][j] (- beta p[j]); zero in the padding [n, n_pad).
@@ -1280,26 +1329,19 @@ k_cgs2_tile(CgsCoopArgs a) {
 // of L2 reads, cheaper than a second barrier), the partial buffers
 // ping-pong between passes, and beta^2 = ||x||^2 - ||c||^2 comes with the
 // last pass's dot products (direct-norm round only when that would cancel).
-template <int MAXE>
-__global__ void __launch_bounds__(kThreads, 1)
-k_cgs2_tile2(CgsCoopArgs a) {
-  unsigned long long t_entry = 0;
-  if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0)
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_entry));
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ double tred[kWarps][32 * MAXE];
-  __shared__ __align__(8) unsigned long long mbar;
-  __shared__ double nacc;
+// k_cgs2_tile2 in two device functions, so the persistent streaming kernel
+// (stream.cuh) runs the same CGS2 inside its step loop: tile2_issue starts
+// the bulk copy of this CTA's basis tile, tile2_rest does the rest.  Every
+// load of data another CTA may have written in the same launch goes through
+// L2 (__ldcg / volatile), and the tile copy is fenced against the generic
+// proxy (fence.proxy.async) -- needed once the kernel is persistent.
+__device__ __forceinline__ void tile2_issue(const CgsCoopArgs& a, double* tile, uint32_t bar,
+                                            bool init) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned G = gridDim.x;
   const int64_t s0 = (int64_t)blockIdx.x * a.rows_per_cta;
   const int64_t s1 = min(a.L, s0 + a.rows_per_cta);
   const int nr = s1 > s0 ? (int)(s1 - s0) : 0;
   const int ldt = (nr + 1) & ~1;  // 16-byte column segments
-  double* tile = reinterpret_cast<double*>(smem_raw);
-  double* cs = tile + (size_t)a.ncols * ldt;  // coefficients of the current pass
-  const uint32_t bar = smem_u32(&mbar);
-
   // bulk-async load of the basis tile: lane 0 of warp 0 arms the mbarrier
   // with the total byte count, then the 32 lanes of warp 0 issue the
   // per-column copies (one thread issuing ~100+ copies serially was the
@@ -1307,15 +1349,18 @@ k_cgs2_tile2(CgsCoopArgs a) {
   if (warp == 0) {
     const uint32_t bytes = (uint32_t)ldt * 8u;
     if (lane == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      if (init) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
       const uint32_t total = bytes * (uint32_t)a.ncols;
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
                    "r"(total)
                    : "memory");
     }
     __syncwarp();
-    if (bytes)
+    if (bytes) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
       for (int j = lane; j < a.ncols; j += 32) {
         const double* src = a.B + (int64_t)j * a.ldb + s0;
         asm volatile(
@@ -1324,23 +1369,27 @@ k_cgs2_tile2(CgsCoopArgs a) {
             "l"(src), "r"(bytes), "r"(bar)
             : "memory");
       }
+    }
   }
-  // The basis columns were written >= 2 launches back (complete once the
-  // predecessor passed its own pdl_wait), so the tile copy above may run
-  // ahead of this wait; the partial sums / x below may not.
-  pdl_wait();
-  pdl_trigger(2);
-  if (halted(a.st)) {  // drain the copy into this CTA's smem before exiting
-    if (threadIdx.x == 0)
-      while (!mbar_try_wait(bar, 0)) {
-      }
-    return;
-  }
+}
+
+template <int MAXE>
+__device__ __forceinline__ void tile2_rest(const CgsCoopArgs& a, double* tile,
+                                           double (*tred)[32 * MAXE], uint32_t bar,
+                                           uint32_t parity, unsigned long long t_entry) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned G = gridDim.x;
+  const int64_t s0 = (int64_t)blockIdx.x * a.rows_per_cta;
+  const int64_t s1 = min(a.L, s0 + a.rows_per_cta);
+  const int nr = s1 > s0 ? (int)(s1 - s0) : 0;
+  const int ldt = (nr + 1) & ~1;
+  double* cs = tile + (size_t)a.ncols * ldt;  // coefficients of the current pass
   // [0] finalisation of the split partial sums of A^T q (overlaps the copy)
   if (a.fpart) {
+    const double fb = a.fp ? __ldcg(a.fbeta) : 0.0;
     for (int64_t r = s0 + threadIdx.x; r < s1; r += kThreads) {
       double v = strided_sum(a.fpart + r, a.fld, a.fnsplit);
-      if (a.fp) v = v - (*a.fbeta) * a.fp[r];
+      if (a.fp) v = v - fb * __ldcg(a.fp + r);
       a.x[r] = v;
       flag_nonfinite(a.st, v, a.step);
     }
@@ -1357,7 +1406,7 @@ k_cgs2_tile2(CgsCoopArgs a) {
     const int rl = lane + 32 * e;
     xv[e] = rl < nr ? a.x[s0 + rl] : 0.0;
   }
-  while (!mbar_try_wait(bar, 0)) {
+  while (!mbar_try_wait(bar, parity)) {
   }
   phase_mark(a.tdbg, 1, tl);  // [1] bulk copy of the tile (+ finalisation)
 
@@ -1467,7 +1516,8 @@ k_cgs2_tile2(CgsCoopArgs a) {
       const double nrm = sqrt(nrm2);
       *a.slot = nrm;
       int stop = ST_RUNNING;
-      if (a.st->nonfinite || !isfinite(nrm)) stop = ST_NONFINITE;
+      if (*reinterpret_cast<volatile int*>(&a.st->nonfinite) || !isfinite(nrm))
+        stop = ST_NONFINITE;
       else if (nrm < a.eps) stop = a.code;
       if (stop != ST_RUNNING) {
         a.st->status = stop;
@@ -1539,6 +1589,32 @@ k_cgs2_tile2(CgsCoopArgs a) {
     atomicAdd(a.tdbg + 6, now - t_entry);
     atomicAdd(a.tdbg + 7, 1ull);
   }
+}
+
+template <int MAXE>
+__global__ void __launch_bounds__(kThreads, 1)
+k_cgs2_tile2(CgsCoopArgs a) {
+  unsigned long long t_entry = 0;
+  if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0)
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_entry));
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ double tred[kWarps][32 * MAXE];
+  __shared__ __align__(8) unsigned long long mbar;
+  double* tile = reinterpret_cast<double*>(smem_raw);
+  const uint32_t bar = smem_u32(&mbar);
+  tile2_issue(a, tile, bar, true);
+  // The basis columns were written >= 2 launches back (complete once the
+  // predecessor passed its own pdl_wait), so the tile copy above may run
+  // ahead of this wait; the partial sums / x below may not.
+  pdl_wait();
+  pdl_trigger(2);
+  if (halted(a.st)) {  // drain the copy into this CTA's smem before exiting
+    if (threadIdx.x == 0)
+      while (!mbar_try_wait(bar, 0)) {
+      }
+    return;
+  }
+  tile2_rest<MAXE>(a, tile, tred, bar, 0, t_entry);
 }
 
 
