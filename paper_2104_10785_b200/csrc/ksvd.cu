@@ -30,6 +30,7 @@
 #include "klrm.cuh"
 #include "resident.cuh"
 #include "peer.cuh"
+#include "stream.cuh"
 #include "ksvd.h"
 
 using namespace ksvd;
@@ -1025,6 +1026,157 @@ static int set_l2_window(ksvd_mat* M, bool on) {
 
 static int run_steps(ksvd_run* R, int i0);
 
+// ---------------------------------------------------------------------------
+// Persistent streaming kernel (stream.cuh): single rank, f64, the gemv_n
+// plan at one CTA per SM, a gemv_t plan with 8 row groups; runs steps
+// 1..i_end where both CGS2 basis tiles still fit shared memory, then (if the
+// run has not stopped) the 4-launch loop continues at i_end + 1.
+// Opt-in (KSVD_STREAM=1): measured on config 2 (CTA-0 phase times per step)
+// the two CGS2 phases drop from ~48 to ~39 us, but A^T q at one CTA per SM
+// takes 152 us against 117 us for the standalone k_gemv_t2 at four CTAs per
+// SM (loads in flight), so the 4-launch loop stays the default.
+static bool stream_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("KSVD_STREAM");
+    return e && strcmp(e, "1") == 0;
+  }();
+  return on;
+}
+
+static size_t tile_bytes_for(int64_t rows, int ncols) {
+  const int64_t ldt = (rows + 1) & ~(int64_t)1;
+  return sizeof(double) * ((size_t)ncols * ldt + ncols + 2) + 16;
+}
+
+template <int MAXE, int ITT>
+static int stream_attr(size_t smem) {
+  CK(cudaFuncSetAttribute(k_gk_stream<MAXE, ITT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  return 0;
+}
+
+static int run_stream(ksvd_run* R, int* i0) {
+  ksvd_mat* M = R->M;
+  ksvd_ctx* c = M->ctx;
+  if (!stream_enabled() || c->comm || M->fac || M->dtype != KSVD_F64 || M->mloc == 0)
+    return 0;
+  const int64_t G = c->sms;
+  if (M->pn.blocks > G || M->pt.rg != 8) return 0;
+  const int64_t rows_l = rup(cdiv(M->mloc, G), 2), rows_r = rup(cdiv(M->n, G), 2);
+  if (rows_l > 256 || rows_r > 256) return 0;
+  // dynamic tile budget: leave room for the kernel's static shared memory
+  // (CGS row sums, gemv_t q staging and group sums: <= 28 KB) under 227 KB
+  constexpr size_t kStreamTileMax = kTileSmemMax - 32 * 1024;
+  int i_end = 0;
+  for (int i = 1; i <= R->k_max; ++i) {
+    if (tile_bytes_for(rows_l, i) > kStreamTileMax || tile_bytes_for(rows_r, i) > kStreamTileMax)
+      break;
+    i_end = i;
+  }
+  if (i_end < 8) return 0;  // too few steps to be worth a launch
+  const size_t smem = std::max(tile_bytes_for(rows_l, i_end), tile_bytes_for(rows_r, i_end));
+  TRY(grow_bases(R, i_end + 1 <= R->k_max ? i_end + 1 : i_end));
+  TRY(ensure_cgs(c->stream, &R->left, G, 2 * (i_end + 2)));
+  TRY(ensure_cgs(c->stream, &R->right, G, 2 * (i_end + 2)));
+  static const int64_t red_max = [] {
+    const char* e = getenv("KSVD_RED_MAX");
+    return e ? (int64_t)atoll(e) : (int64_t)148 * 16;
+  }();
+  StreamArgs a{};
+  a.A = (const double*)M->A;
+  a.lda = M->lda;
+  a.mloc = M->mloc;
+  a.n = M->n;
+  a.nvec = M->pn.nvec;
+  a.nchunks = M->pn.nchunks;
+  a.nseg = M->pn.rows_per_warp;
+  a.part_n = M->part_n;
+  a.ncoltiles = M->pt.ncoltiles;
+  a.nsplit = M->pt.nsplit;
+  a.ldz = M->n_pad;
+  a.part_t = M->part_t;
+  a.Q = R->Q;
+  a.P = R->P;
+  a.ldq = R->ldq;
+  a.ldp = R->ldp;
+  a.w = R->w;
+  a.z = R->z;
+  a.alpha = R->alpha;
+  a.beta = R->beta;
+  a.st = R->st;
+  a.i0 = 1;
+  a.i_end = i_end;
+  a.k_max = R->k_max;
+  a.passes = R->reorth;
+  a.eps = R->eps;
+  a.rows_l = (int)rows_l;
+  a.rows_r = (int)rows_r;
+  a.lpart = R->left.part;
+  a.lc = R->left.c;
+  a.lbar = R->left.bar;
+  a.rpart = R->right.part;
+  a.rc = R->right.c;
+  a.rbar = R->right.bar;
+  a.red_max = red_max;
+  a.hp = c->dprog;
+  a.tdbg = c->tdbg;
+  void* args[] = {&a};
+  const bool big = (size_t)M->mloc * M->lda * sizeof(double) >= ((size_t)2 << 30);
+  const int maxe = (int)cdiv(std::max(rows_l, rows_r), 32);
+  const void* kern = nullptr;
+#define KSVD_STREAM_CASE(E)                                                  \
+  case E:                                                                    \
+    if (big) {                                                               \
+      TRY((stream_attr<E, 8>(smem)));                                        \
+      kern = (const void*)k_gk_stream<E, 8>;                                 \
+    } else {                                                                 \
+      TRY((stream_attr<E, 2>(smem)));                                        \
+      kern = (const void*)k_gk_stream<E, 2>;                                 \
+    }                                                                        \
+    break;
+  switch (maxe) {
+    KSVD_STREAM_CASE(1)
+    KSVD_STREAM_CASE(2)
+    KSVD_STREAM_CASE(3)
+    KSVD_STREAM_CASE(4)
+    KSVD_STREAM_CASE(5)
+    KSVD_STREAM_CASE(6)
+    KSVD_STREAM_CASE(7)
+    default:
+      KSVD_STREAM_CASE(8)
+  }
+#undef KSVD_STREAM_CASE
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->profiling) {
+    TRY(get_event(c, &e0));
+    TRY(get_event(c, &e1));
+    CK(cudaEventRecord(e0, c->stream));
+  }
+  const cudaError_t e =
+      cudaLaunchCooperativeKernel(kern, dim3((unsigned)G), dim3(kThreads), args, smem, c->stream);
+  if (e != cudaSuccess)
+    return set_err(KSVD_ERUNTIME, "persistent GK launch: %s", cudaGetErrorString(e));
+  if (c->profiling) {
+    CK(cudaEventRecord(e1, c->stream));
+    c->pending.push_back({e0, e1, KC_RESIDENT});
+  }
+  c->launches++;
+  if (c->tdbg) {
+    unsigned long long t[8];
+    CK(cudaMemcpyAsync(t, c->tdbg, sizeof t, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    fprintf(stderr, "[ksvd] stream phases (us, CTA 0, cumulative): gemv_n %.1f cgs_left %.1f "
+            "gemv_t %.1f cgs_right %.1f\n", t[0] * 1e-3, t[1] * 1e-3, t[2] * 1e-3, t[3] * 1e-3);
+    CK(cudaMemsetAsync(c->tdbg, 0, sizeof t, c->stream));
+  }
+  // continue with the 4-launch loop only if the run is still going
+  DevState h{};
+  CK(cudaMemcpyAsync(&h, R->st, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  *i0 = (h.status == ST_RUNNING && i_end < R->k_max) ? i_end + 1 : R->k_max + 1;
+  return 0;
+}
+
 static int run_loop(ksvd_run* R, const double* q1_local) {
   ksvd_mat* M = R->M;
   ksvd_ctx* c = M->ctx;
@@ -1037,7 +1189,10 @@ static int run_loop(ksvd_run* R, const double* q1_local) {
   TRY(enqueue_gemv_t(M, R->Q, nullptr, nullptr, nullptr, nullptr, R->z, R->st, 0, true));
   TRY(cgs(c, &R->right, R->P, R->ldp, 0, R->z, M->n, 0, false, R->eps, R->alpha + 1, R->st,
           0, ST_DEGENERATE, R->M->ctx->dprog, 1));
-  return run_steps(R, 1);
+  int i0 = 1;
+  TRY(run_stream(R, &i0));  // persistent kernel for the steps whose tiles fit
+  if (i0 > R->k_max) return read_state(R);
+  return run_steps(R, i0);
 }
 
 // GK steps i0..k_max (step i: A p_i and A^T q_{i+1} with their CGS2)
