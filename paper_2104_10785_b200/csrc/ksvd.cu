@@ -239,6 +239,7 @@ static int allreduce(ksvd_ctx* c, double* buf, size_t count) {
 // matrices
 struct GemvNPlan {
   int V, U, nchunks;
+  int pf = 0;  // k_gemv_n2 PF: bulk L2 prefetch one row block ahead (large A)
   int64_t nvec, rows_per_warp, blocks;
 };
 struct GemvTPlan {
@@ -290,11 +291,21 @@ static int plan_matrix(ksvd_mat* M) {
   const int64_t bytes = esize(M->dtype);
   GemvNPlan& pn = M->pn;
   pn.V = (int)(16 / bytes);
-  pn.U = M->dtype == KSVD_F32 ? kUnrollN32 : kUnrollN64;
+  // KSVD_GEMVN_PF=1: U = 4 with the one-block bulk L2 prefetch.  At full
+  // clocks (tools/gemv_bench.cu) it lifts f32 40 GB from 6.62 to 6.85 TB/s
+  // and f64 32 GB from 6.86 to 6.96, but in the long runs of configs 3-4,
+  // under sw_power_cap at ~1.48 GHz, it measured 3-4 % SLOWER (config 4
+  // gemv_n 6.22 vs 6.50 TB/s, config 3 6.72 vs 6.91; tools/pf_ab.sh), so it
+  // is off by default.
+  pn.pf = 0;
+  if (const char* e = getenv("KSVD_GEMVN_PF")) pn.pf = atoi(e) ? 1 : 0;
+  pn.U = M->dtype == KSVD_F32 ? (pn.pf ? 4 : kUnrollN32) : kUnrollN64;
   pn.nvec = cdiv(M->n, pn.V);
   pn.nchunks = (int)cdiv(pn.nvec, 32 * pn.U);
   int occ = 1;
-  if (M->dtype == KSVD_F32)
+  if (M->dtype == KSVD_F32 && pn.U == 4)
+    TRY((occupancy_n2<float, 4>(&occ)));
+  else if (M->dtype == KSVD_F32)
     TRY((occupancy_n2<float, kUnrollN32>(&occ)));
   else
     TRY((occupancy_n2<double, kUnrollN64>(&occ)));
@@ -386,15 +397,24 @@ static int dense_gemv_n(ksvd_mat* M, const double* p_src, const double* p_scale,
   const GemvNPlan& pn = M->pn;
   if (M->mloc == 0) return 0;
   const dim3 grid((unsigned)pn.blocks);
+#define KSVD_GEMVN(TA, U, PF)                                                              \
+  TRY(launch_step(c, KC_GEMV_N, k_gemv_n2<TA, U, 8, PF>, grid, dim3(kThreads), 0,          \
+                  (const TA*)M->A, M->lda, M->mloc, pn.nvec, pn.nchunks, pn.rows_per_warp, \
+                  p_src, p_scale, p_dst, M->n, M->part_n, (const DevState*)st))
   if (M->dtype == KSVD_F32) {
-    TRY(launch_step(c, KC_GEMV_N, k_gemv_n2<float, kUnrollN32>, grid, dim3(kThreads), 0,
-               (const float*)M->A, M->lda, M->mloc, pn.nvec, pn.nchunks, pn.rows_per_warp,
-               p_src, p_scale, p_dst, M->n, M->part_n, (const DevState*)st));
+    if (pn.U == 4)
+      KSVD_GEMVN(float, 4, 1);
+    else if (pn.pf)
+      KSVD_GEMVN(float, kUnrollN32, 1);
+    else
+      KSVD_GEMVN(float, kUnrollN32, 0);
   } else {
-    TRY(launch_step(c, KC_GEMV_N, k_gemv_n2<double, kUnrollN64>, grid, dim3(kThreads), 0,
-               (const double*)M->A, M->lda, M->mloc, pn.nvec, pn.nchunks, pn.rows_per_warp,
-               p_src, p_scale, p_dst, M->n, M->part_n, (const DevState*)st));
+    if (pn.pf)
+      KSVD_GEMVN(double, kUnrollN64, 1);
+    else
+      KSVD_GEMVN(double, kUnrollN64, 0);
   }
+#undef KSVD_GEMVN
   if (finalize)
     TRY(launch(c, KC_FIN, k_gemv_n_finalize, dim3((unsigned)cdiv(M->mloc, kThreads)),
                dim3(kThreads), 0, (const double*)M->part_n, M->mloc, pn.nchunks, M->mloc,

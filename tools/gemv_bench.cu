@@ -151,7 +151,13 @@ void suite(int64_t m, int64_t n, int sms) {
   cudaMalloc(&st, sizeof(DevState));
   cudaMemset(st, 0, sizeof(DevState));
   time_n2<TA, 4, 8, 0>(A, lda, m, n, p, part, st, sms, 8);
+  time_n2<TA, 4, 8, 1>(A, lda, m, n, p, part, st, sms, 8);
+  time_n2<TA, 4, 8, 2>(A, lda, m, n, p, part, st, sms, 8);
+  time_n2<TA, 4, 8, 4>(A, lda, m, n, p, part, st, sms, 8);
+  time_n2<TA, 4, 16, 0>(A, lda, m, n, p, part, st, sms, 8);
   time_n2<TA, 2, 8, 0>(A, lda, m, n, p, part, st, sms, 8);
+  time_n2<TA, 2, 16, 0>(A, lda, m, n, p, part, st, sms, 8);
+  time_n2<TA, 2, 8, 2>(A, lda, m, n, p, part, st, sms, 8);
   timet<TA, 16, 8>(A, lda, m, n, w, part, st, sms, 4);
   timet2<TA, 16, 8, 1>(A, lda, m, n, w, part, st, sms, 4);
   timet2<TA, 16, 8, 2>(A, lda, m, n, w, part, st, sms, 4);
