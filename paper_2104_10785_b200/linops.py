@@ -288,10 +288,25 @@ def as_operator(A) -> DeviceMatrix:
             f"{type(A).__name__} is a host-side operator; the B200 path needs a dense "
             "matrix (ndarray, CUDA tensor or DeviceMatrix) -- there is no CPU fallback")
     try:
-        import torch  # noqa: F401
+        import torch
 
-        if hasattr(A, "is_cuda") and A.is_cuda:
-            return DeviceMatrix.from_torch(A)
+        if isinstance(A, torch.Tensor) and A.is_cuda:
+            # device-to-device copy of this rank's row shard (any layout,
+            # any real dtype: made row-major f64 / f32 on the device first)
+            if A.dim() != 2:
+                raise ShapeMismatchError(f"expected a 2-d matrix, got shape {tuple(A.shape)}")
+            ctx = _lib.get_context()
+            t = A
+            if t.device.index != ctx.device:
+                t = t.to(f"cuda:{ctx.device}")
+            if t.dtype not in (torch.float64, torch.float32):
+                t = t.to(torch.float64)
+            m = int(t.shape[0])
+            r0, ml = row_partition(m, ctx.nranks, ctx.rank)
+            t = t[r0:r0 + ml]
+            if t.dim() != 2 or (ml > 0 and t.stride(1) != 1) or (ml > 1 and t.stride(0) < t.shape[1]):
+                t = t.contiguous()
+            return DeviceMatrix.from_torch(t, ctx=ctx, row0=r0, m_global=m)
     except ImportError:
         pass
     A = np.asarray(A)
