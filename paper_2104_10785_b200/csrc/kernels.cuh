@@ -1373,8 +1373,10 @@ __device__ __forceinline__ void tile2_issue(const CgsCoopArgs& a, double* tile, 
   }
 }
 
+// Returns ||x||^2 after the orthogonalisation (the same value in every CTA:
+// callers of the persistent kernels use it instead of re-reading the slot).
 template <int MAXE>
-__device__ __forceinline__ void tile2_rest(const CgsCoopArgs& a, double* tile,
+__device__ __forceinline__ double tile2_rest(const CgsCoopArgs& a, double* tile,
                                            double (*tred)[32 * MAXE], uint32_t bar,
                                            uint32_t parity, unsigned long long t_entry) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1511,7 +1513,9 @@ __device__ __forceinline__ void tile2_rest(const CgsCoopArgs& a, double* tile,
     }
     __syncthreads();
   };
+  double result = 0.0;
   auto finish = [&](double nrm2) {
+    result = nrm2;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       const double nrm = sqrt(nrm2);
       *a.slot = nrm;
@@ -1589,6 +1593,7 @@ __device__ __forceinline__ void tile2_rest(const CgsCoopArgs& a, double* tile,
     atomicAdd(a.tdbg + 6, now - t_entry);
     atomicAdd(a.tdbg + 7, 1ull);
   }
+  return result;
 }
 
 template <int MAXE>

@@ -1197,6 +1197,135 @@ static int run_stream(ksvd_run* R, int* i0) {
   return 0;
 }
 
+// Row-streamed persistent kernel (stream.cuh k_gk_rows): A's rows through a
+// bulk-copy ring in shared memory, 2 grid barriers per step besides the
+// CGS2 rounds.  KSVD_ROWS=1 enables it (single rank, f64, n <= 6144).
+static bool rows_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("KSVD_ROWS");
+    return e && strcmp(e, "1") == 0;
+  }();
+  return on;
+}
+
+template <int MAXE>
+static int rows_attr(size_t smem) {
+  CK(cudaFuncSetAttribute(k_gk_rows<MAXE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  return 0;
+}
+
+static int run_rows(ksvd_run* R, int* i0) {
+  ksvd_mat* M = R->M;
+  ksvd_ctx* c = M->ctx;
+  if (!rows_enabled() || c->comm || M->fac || M->dtype != KSVD_F64 || M->mloc == 0) return 0;
+  const int64_t G = c->sms;
+  if (M->n > (int64_t)kThreads * kRowCols) return 0;
+  const int64_t rows_l = rup(cdiv(M->mloc, G), 2), rows_r = rup(cdiv(M->n, G), 2);
+  if (rows_l > 256 || rows_r > 256) return 0;
+  constexpr size_t kBudget = kTileSmemMax - 32 * 1024;  // + ~30 KB static
+  const size_t ring = sizeof(double) * kRowRing * (size_t)rup(M->n, 2);
+  if (ring > kBudget) return 0;
+  int i_end = 0;
+  for (int i = 1; i <= R->k_max; ++i) {
+    if (tile_bytes_for(rows_l, i) > kBudget || tile_bytes_for(rows_r, i) > kBudget) break;
+    i_end = i;
+  }
+  if (i_end < 8) return 0;
+  const size_t smem =
+      std::max({ring, tile_bytes_for(rows_l, i_end), tile_bytes_for(rows_r, i_end)});
+  TRY(grow_bases(R, i_end + 1 <= R->k_max ? i_end + 1 : i_end));
+  TRY(ensure_cgs(c->stream, &R->left, G, 2 * (i_end + 2)));
+  TRY(ensure_cgs(c->stream, &R->right, G, 2 * (i_end + 2)));
+  double* zpart = nullptr;
+  CK(cudaMallocAsync(&zpart, sizeof(double) * G * M->n_pad, c->stream));
+  static const int64_t red_max = [] {
+    const char* e = getenv("KSVD_RED_MAX");
+    return e ? (int64_t)atoll(e) : (int64_t)148 * 16;
+  }();
+  RowsArgs a{};
+  a.A = (const double*)M->A;
+  a.lda = M->lda;
+  a.mloc = M->mloc;
+  a.n = M->n;
+  a.ldz = M->n_pad;
+  a.Q = R->Q;
+  a.P = R->P;
+  a.ldq = R->ldq;
+  a.ldp = R->ldp;
+  a.w = R->w;
+  a.z = R->z;
+  a.alpha = R->alpha;
+  a.beta = R->beta;
+  a.zpart = zpart;
+  a.st = R->st;
+  a.i0 = 1;
+  a.i_end = i_end;
+  a.k_max = R->k_max;
+  a.passes = R->reorth;
+  a.eps = R->eps;
+  a.rows_l = (int)rows_l;
+  a.rows_r = (int)rows_r;
+  a.lpart = R->left.part;
+  a.lc = R->left.c;
+  a.lbar = R->left.bar;
+  a.rpart = R->right.part;
+  a.rc = R->right.c;
+  a.rbar = R->right.bar;
+  a.red_max = red_max;
+  a.hp = c->dprog;
+  a.tdbg = c->tdbg;
+  void* args[] = {&a};
+  const int maxe = (int)cdiv(std::max(rows_l, rows_r), 32);
+  const void* kern = nullptr;
+#define KSVD_ROWS_CASE(E)                      \
+  case E:                                      \
+    TRY(rows_attr<E>(smem));                   \
+    kern = (const void*)k_gk_rows<E>;          \
+    break;
+  switch (maxe) {
+    KSVD_ROWS_CASE(1)
+    KSVD_ROWS_CASE(2)
+    KSVD_ROWS_CASE(3)
+    KSVD_ROWS_CASE(4)
+    KSVD_ROWS_CASE(5)
+    KSVD_ROWS_CASE(6)
+    KSVD_ROWS_CASE(7)
+    default:
+      KSVD_ROWS_CASE(8)
+  }
+#undef KSVD_ROWS_CASE
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->profiling) {
+    TRY(get_event(c, &e0));
+    TRY(get_event(c, &e1));
+    CK(cudaEventRecord(e0, c->stream));
+  }
+  const cudaError_t e =
+      cudaLaunchCooperativeKernel(kern, dim3((unsigned)G), dim3(kThreads), args, smem, c->stream);
+  cudaFreeAsync(zpart, c->stream);
+  if (e != cudaSuccess)
+    return set_err(KSVD_ERUNTIME, "row-streamed GK launch: %s", cudaGetErrorString(e));
+  if (c->profiling) {
+    CK(cudaEventRecord(e1, c->stream));
+    c->pending.push_back({e0, e1, KC_RESIDENT});
+  }
+  c->launches++;
+  if (c->tdbg) {
+    unsigned long long t[8];
+    CK(cudaMemcpyAsync(t, c->tdbg, sizeof t, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    fprintf(stderr, "[ksvd] rows phases (us, CTA 0, cumulative): gemv_n %.1f cgs_left %.1f "
+            "gemv_t %.1f cgs_right %.1f\n", t[0] * 1e-3, t[1] * 1e-3, t[2] * 1e-3, t[3] * 1e-3);
+    CK(cudaMemsetAsync(c->tdbg, 0, sizeof t, c->stream));
+  }
+  DevState h{};
+  CK(cudaMemcpyAsync(&h, R->st, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  *i0 = (h.status == ST_RUNNING && i_end < R->k_max) ? i_end + 1 : R->k_max + 1;
+  return 0;
+}
+
 static int run_loop(ksvd_run* R, const double* q1_local) {
   ksvd_mat* M = R->M;
   ksvd_ctx* c = M->ctx;
@@ -1210,7 +1339,8 @@ static int run_loop(ksvd_run* R, const double* q1_local) {
   TRY(cgs(c, &R->right, R->P, R->ldp, 0, R->z, M->n, 0, false, R->eps, R->alpha + 1, R->st,
           0, ST_DEGENERATE, R->M->ctx->dprog, 1));
   int i0 = 1;
-  TRY(run_stream(R, &i0));  // persistent kernel for the steps whose tiles fit
+  TRY(run_rows(R, &i0));  // row-streamed persistent kernel (n <= 6144)
+  if (i0 == 1) TRY(run_stream(R, &i0));  // persistent kernel for the steps whose tiles fit
   if (i0 > R->k_max) return read_state(R);
   return run_steps(R, i0);
 }

@@ -286,6 +286,7 @@ _MULTI = {"KSVD_RESIDENT": "0"}  # small cases would otherwise take the resident
                                  {"KSVD_CGS_SYNC": "5", **_MULTI}, {"KSVD_RED_MAX": "0", **_MULTI},
                                  {"KSVD_RED_MAX": "100000000", **_MULTI}, {"KSVD_PDL": "0", **_MULTI},
                                  {"KSVD_PDL_TRIG": "3", **_MULTI}, {"KSVD_STREAM": "1", **_MULTI},
+                                 {"KSVD_ROWS": "1", **_MULTI},
                                  _MULTI, {}])
 def test_cgs_paths_agree(env):
     """The whole-loop resident kernel (small matrices, default), the tile-resident (2-round k_cgs2_tile2 with redundant or distributed
