@@ -939,8 +939,32 @@ struct CgsCoopArgs {
 // Grid-wide barrier of the cooperative launch (cooperative_groups: ~1.2 us
 // on 148 SMs, measured by tools/barrier_bench.cu, vs ~2.3 us for a plain
 // counter/generation barrier).
-__device__ __forceinline__ void grid_barrier(unsigned* /*bar*/, unsigned /*nblocks*/) {
-  cooperative_groups::this_grid().sync();
+// bar == nullptr: cooperative-groups grid sync (cooperative launch).
+// Otherwise a sense-reversal barrier on {count, generation} for a regular
+// launch whose CTAs are all resident (one per SM, see cgs_coop): lets the
+// CGS grid start under programmatic dependent launch, which a cooperative
+// launch does not.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
+  if (bar == nullptr) {
+    cooperative_groups::this_grid().sync();
+    return;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
 }
 
 // phase timestamps of CTA 0 (debug builds of the timing breakdown)

@@ -808,18 +808,35 @@ static int cgs_coop(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int n
     CK(cudaEventRecord(e0, c->stream));
   }
   {
+    // KSVD_COOP_LAUNCH=0 (experiment): a regular launch with the custom
+    // grid barrier, so programmatic dependent launch can start the grid
+    // while the product drains (all G <= #SMs CTAs become resident once it
+    // has: the CGS tile takes an SM's shared memory, one CTA per SM)
+    static const bool regular = [] {
+      const char* e = getenv("KSVD_COOP_LAUNCH");
+      return e && strcmp(e, "0") == 0;
+    }();
+    const bool reg = regular && G <= c->sms;
+    if (!reg) a.bar = nullptr;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)G);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c->stream;
     cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
+    int na = 0;
+    if (!reg) {
+      at[na].id = cudaLaunchAttributeCooperative;
+      at[na].val.cooperative = 1;
+      ++na;
+    }
+    if (pdl_enabled(c)) {
+      at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[na].val.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled(c) ? 2 : 1;
+    cfg.numAttrs = na;
     CK(cudaLaunchKernelExC(&cfg, kern, args));
   }
   if (c->profiling) {
