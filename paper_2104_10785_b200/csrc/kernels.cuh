@@ -783,17 +783,27 @@ k_cgs_rows(const double* __restrict__ B, int64_t ldb, int ncols,
     }
   }
   if (mode & kDot) {
-#pragma unroll 2
-    for (int j = warp; j < ncols; j += kWarps) {
-      const double* col = B + (int64_t)j * ldb;
-      double s = 0.0;
+    // 8 columns per batch: 8 * RPL independent loads in flight per lane and
+    // one 9-shuffle transpose butterfly (warp_sum8) for the 8 sums, instead
+    // of a 5-shuffle reduction per column (the dot pass was latency-bound)
+    for (int q0 = 0; warp + kWarps * q0 < ncols; q0 += 8) {
+      double v[8];
 #pragma unroll
-      for (int e = 0; e < RPL; ++e) {
-        const int64_t r = r0 + 32 * e;
-        if (r < L) s = fma(col[r], xv[e], s);
+      for (int u = 0; u < 8; ++u) {
+        const int j = warp + kWarps * (q0 + u);
+        v[u] = 0.0;
+        if (j < ncols) {
+          const double* col = B + (int64_t)j * ldb;
+#pragma unroll
+          for (int e = 0; e < RPL; ++e) {
+            const int64_t r = r0 + 32 * e;
+            if (r < L) v[u] = fma(col[r], xv[e], v[u]);
+          }
+        }
       }
-      s = warp_sum(s);
-      if (lane == 0) part[(int64_t)j * nrb + blockIdx.x] = s;
+      const double t = warp_sum8(v);
+      const int j = warp + kWarps * (q0 + warp_sum8_index(lane));
+      if ((lane & 3) == 0 && j < ncols) part[(int64_t)j * nrb + blockIdx.x] = t;
     }
   }
   if ((mode & kNorm) && warp == 0) {
