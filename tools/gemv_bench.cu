@@ -163,6 +163,11 @@ void suite(int64_t m, int64_t n, int sms) {
   timet2<TA, 16, 8, 2>(A, lda, m, n, w, part, st, sms, 4);
   timet2<TA, 16, 8, 8>(A, lda, m, n, w, part, st, sms, 4);
   timet2<TA, 16, 8, 2>(A, lda, m, n, w, part, st, sms, 8);
+  timet2<TA, 16, 8, 2>(A, lda, m, n, w, part, st, sms, 3);
+  timet2<TA, 16, 8, 2>(A, lda, m, n, w, part, st, sms, 6);
+  timet2<TA, 16, 4, 2>(A, lda, m, n, w, part, st, sms, 4);
+  timet2<TA, 32, 8, 1>(A, lda, m, n, w, part, st, sms, 4);
+  timet2<TA, 32, 4, 2>(A, lda, m, n, w, part, st, sms, 4);
   timet2<TA, 8, 8, 4>(A, lda, m, n, w, part, st, sms, 4);
   cudaFree(A);
   cudaFree(p);
@@ -176,7 +181,9 @@ int main(int argc, char** argv) {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   suite<double>(20000, 5000, sms);
-  suite<double>(200000, 20000, sms);
-  suite<float>(250000, 40000, sms);
+  if (argc < 2) {
+    suite<double>(200000, 20000, sms);
+    suite<float>(250000, 40000, sms);
+  }
   return 0;
 }
