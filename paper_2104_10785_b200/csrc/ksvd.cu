@@ -2025,11 +2025,28 @@ int ksvd_px_export(ksvd_ctx* c, int64_t slot, unsigned char* handle) {
   return 0;
 }
 
+// Collective in two agreement rounds over NCCL, so a rank that cannot map a
+// peer (no P2P path, devices hidden by CUDA_VISIBLE_DEVICES, ...) never
+// leaves the others spinning: (1) every rank maps the peers and the ranks
+// agree that all mappings succeeded; (2) only then the exchange runs a
+// self-test against ncclAllReduce and is enabled iff it matched everywhere.
+// Any failure leaves NCCL in charge and is not an error.
+static int px_agree(ksvd_ctx* c, double* dev, bool mine, bool* all) {
+  double v = mine ? 1.0 : 0.0;
+  CK(cudaMemcpy(dev, &v, sizeof v, cudaMemcpyHostToDevice));
+  NK(ncclAllReduce(dev, dev, 1, ncclDouble, ncclSum, c->comm, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(&v, dev, sizeof v, cudaMemcpyDeviceToHost));
+  *all = v == (double)c->nranks;
+  return 0;
+}
+
 int ksvd_px_open(ksvd_ctx* c, const unsigned char* handles) {
   if (!c->px_local) return set_err(KSVD_ECONFIG, "ksvd_px_export first");
   CK(cudaSetDevice(c->device));
   const size_t recv = sizeof(double) * 2 * (size_t)c->nranks * c->px_slot;
-  for (int r = 0; r < c->nranks; ++r) {
+  bool mapped = true;
+  for (int r = 0; r < c->nranks && mapped; ++r) {
     char* base;
     if (r == c->rank) {
       base = static_cast<char*>(c->px_local);
@@ -2037,42 +2054,47 @@ int ksvd_px_open(ksvd_ctx* c, const unsigned char* handles) {
       cudaIpcMemHandle_t h;
       memcpy(&h, handles + (size_t)r * KSVD_PX_HANDLE_BYTES, sizeof h);
       void* p = nullptr;
-      CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();  // clear; reported through the agreement below
+        mapped = false;
+        break;
+      }
       c->px_mapped[r] = p;
       base = static_cast<char*>(p);
     }
     c->px_recv[r] = reinterpret_cast<double*>(base);
     c->px_cnt[r] = reinterpret_cast<unsigned long long*>(base + recv);
   }
-  // self-test against NCCL on every rank; enabled only if it agrees everywhere
   const int64_t L = std::min<int64_t>(c->px_slot, 4099);
   double* v = nullptr;
-  CK(cudaMalloc(&v, sizeof(double) * 2 * L + sizeof(double)));
-  std::vector<double> h0(L), h1(L);
-  for (int64_t i = 0; i < L; ++i) h0[i] = (double)((c->rank + 1) * (i % 97) + 0.25 * i);
-  CK(cudaMemcpy(v, h0.data(), sizeof(double) * L, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(v + L, h0.data(), sizeof(double) * L, cudaMemcpyHostToDevice));
-  int rc = px_allreduce(c, v, (size_t)L);
-  if (!rc) {
-    ncclResult_t nr = ncclAllReduce(v + L, v + L, L, ncclDouble, ncclSum, c->comm, c->stream);
-    if (nr != ncclSuccess) rc = set_err(KSVD_ERUNTIME, "nccl: %s", ncclGetErrorString(nr));
+  CK(cudaMalloc(&v, sizeof(double) * (2 * L + 1)));
+  bool all = false;
+  int rc = px_agree(c, v + 2 * L, mapped, &all);
+  if (!rc && all) {
+    // self-test: exact agreement is expected (small integers and quarters)
+    std::vector<double> h0(L), h1(L);
+    for (int64_t i = 0; i < L; ++i) h0[i] = (double)((c->rank + 1) * (i % 97) + 0.25 * i);
+    CK(cudaMemcpy(v, h0.data(), sizeof(double) * L, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(v + L, h0.data(), sizeof(double) * L, cudaMemcpyHostToDevice));
+    rc = px_allreduce(c, v, (size_t)L);
+    int err = 0;
+    if (!rc) {
+      ncclResult_t nr = ncclAllReduce(v + L, v + L, L, ncclDouble, ncclSum, c->comm, c->stream);
+      if (nr != ncclSuccess) rc = set_err(KSVD_ERUNTIME, "nccl: %s", ncclGetErrorString(nr));
+    }
+    if (!rc) {
+      CK(cudaStreamSynchronize(c->stream));
+      CK(cudaMemcpy(h0.data(), v, sizeof(double) * L, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(h1.data(), v + L, sizeof(double) * L, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(&err, c->px_err, sizeof(int), cudaMemcpyDeviceToHost));
+    }
+    if (!rc) rc = px_agree(c, v + 2 * L, !err && h0 == h1, &all);
   }
-  int err = 0;
-  if (!rc) {
-    CK(cudaStreamSynchronize(c->stream));
-    CK(cudaMemcpy(h0.data(), v, sizeof(double) * L, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(h1.data(), v + L, sizeof(double) * L, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(&err, c->px_err, sizeof(int), cudaMemcpyDeviceToHost));
-  }
-  // exact agreement is expected: small integers and quarters sum exactly
-  double ok = (!rc && !err && h0 == h1) ? 1.0 : 0.0;
-  CK(cudaMemcpy(v, &ok, sizeof(double), cudaMemcpyHostToDevice));
-  NK(ncclAllReduce(v, v, 1, ncclDouble, ncclSum, c->comm, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  CK(cudaMemcpy(&ok, v, sizeof(double), cudaMemcpyDeviceToHost));
   cudaFree(v);
-  c->px = ok == (double)c->nranks;
-  if (!c->px) fprintf(stderr, "[ksvd] peer exchange self-test failed on some rank: using NCCL\n");
+  c->px = !rc && all;
+  if (!c->px)
+    fprintf(stderr, "[ksvd] peer exchange unavailable on some rank (mapping or self-test): "
+            "using NCCL\n");
   return rc;
 }
 

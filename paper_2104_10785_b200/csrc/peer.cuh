@@ -61,8 +61,10 @@ __global__ void __launch_bounds__(kThreads) k_px_allreduce(PxArgs a) {
     const unsigned long long* c = a.my_cnt + (int64_t)threadIdx.x * kPxCntStride;
     long long spins = 0;
     while (ld_acquire_sys(c) < want) {
-      // ~0.5 s: a peer never arrived; once flagged, later calls do not wait
-      if (*reinterpret_cast<volatile int*>(a.err) || ++spins > (1ll << 23)) {
+      // ~a minute: a peer never arrived (a legitimately late peer -- host
+      // work between calls -- is far inside this); once flagged, later
+      // calls do not wait
+      if (*reinterpret_cast<volatile int*>(a.err) || ++spins > (1ll << 30)) {
         atomicExch(a.err, 1);
         break;
       }
@@ -106,7 +108,7 @@ k_gemv_t_fin_px(PxArgs a, const double* __restrict__ part, int64_t ldz, int nspl
     const unsigned long long* c = a.my_cnt + (int64_t)threadIdx.x * kPxCntStride;
     long long spins = 0;
     while (ld_acquire_sys(c) < a.want) {
-      if (*reinterpret_cast<volatile int*>(a.err) || ++spins > (1ll << 23)) {
+      if (*reinterpret_cast<volatile int*>(a.err) || ++spins > (1ll << 30)) {
         atomicExch(a.err, 1);
         break;
       }
