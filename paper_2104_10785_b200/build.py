@@ -58,7 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [
         _nvcc(), ARCH, "-O3", "-std=c++17", "-lineinfo", "-shared",
-        "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
+        "-Xcompiler", "-fPIC,-ffp-contract=off,-O3",
         "-Xptxas", "-v" if verbose else "-O3",
         f"-I{INCLUDE}", f"-I{CSRC}", f"-I{inc}",
         *[str(s) for s in SOURCES],

@@ -188,24 +188,66 @@ extern "C" int ksvd_bidiag_sv2(int k, const double* alphas, const double* betas,
   const double tau = 1e-6 * std::max(th[0], 0.0);
   int tail = 0;
   while (tail < k && th[k - 1 - tail] < tau) ++tail;
-  for (int j = 0; j < tail; ++j) {  // j-th smallest singular value
-    double lo = 0.0, hi = gersh * (1.0 + 4 * DBL_EPSILON) + DBL_MIN;
-    for (int it = 0; it < 400; ++it) {
-      if (hi - lo <= 4 * DBL_EPSILON * hi || hi < 1e-300) break;
-      double mid;
-      if (lo == 0.0)
-        mid = hi * (hi > 1e-280 ? 1e-3 : 0.5);  // coarse descent to the scale
-      else if (hi > 2.0 * lo)
-        mid = std::sqrt(lo * hi);  // geometric bisection
-      else
-        mid = 0.5 * (lo + hi);
-      if (t.below(mid) <= j)
-        lo = mid;
-      else
-        hi = mid;
+  // Upper end of the tail bracket: every tail value is below sqrt(tau) up to
+  // QL's absolute error; verified with one Sturm count (else Gershgorin).
+  double top = std::sqrt(tau + 64.0 * DBL_EPSILON * std::max(th[0], 0.0)) * (1.0 + 1e-8);
+  if (tail > 0 && t.below(top) < tail) top = gersh * (1.0 + 4 * DBL_EPSILON) + DBL_MIN;
+  // Bisection of up to kLanes tail values in lock step: one pass over the
+  // TGK entries advances every lane's Sturm count (independent dependency
+  // chains, so the division latency overlaps).  Lane j bisects the j-th
+  // smallest value; the same per-lane steps as a scalar bisection.
+  constexpr int kLanes = 8;
+  for (int j0 = 0; j0 < tail; j0 += kLanes) {
+    const int nl = std::min(kLanes, tail - j0);
+    double lo[kLanes], hi[kLanes], mid[kLanes];
+    bool live[kLanes];
+    for (int l = 0; l < kLanes; ++l) {
+      lo[l] = 0.0;
+      hi[l] = top;
+      live[l] = l < nl;
     }
-    const double sv = 0.5 * (lo + hi);
-    th[k - 1 - j] = sv * sv;
+    for (int it = 0; it < 400; ++it) {
+      bool any = false;
+      for (int l = 0; l < nl; ++l) {
+        if (live[l] && (hi[l] - lo[l] <= 4 * DBL_EPSILON * hi[l] || hi[l] < 1e-300)) live[l] = false;
+        if (!live[l]) continue;
+        any = true;
+        if (lo[l] == 0.0)
+          mid[l] = hi[l] * (hi[l] > 1e-280 ? 1e-3 : 0.5);  // coarse descent to the scale
+        else if (hi[l] > 2.0 * lo[l])
+          mid[l] = std::sqrt(lo[l] * hi[l]);  // geometric bisection
+        else
+          mid[l] = 0.5 * (lo[l] + hi[l]);
+      }
+      if (!any) break;
+      double q[kLanes];
+      int neg[kLanes];
+      for (int l = 0; l < kLanes; ++l) {
+        const double x = live[l] ? mid[l] : 1.0;
+        q[l] = -x;
+        neg[l] = q[l] < 0;
+      }
+      for (double v : t.e2) {
+        for (int l = 0; l < kLanes; ++l) {
+          const double x = live[l] ? mid[l] : 1.0;
+          double ql = -x - v / q[l];
+          if (std::fabs(ql) < t.pivmin) ql = -t.pivmin;
+          q[l] = ql;
+          neg[l] += ql < 0;
+        }
+      }
+      for (int l = 0; l < nl; ++l) {
+        if (!live[l]) continue;
+        if (neg[l] - (k + 1) <= j0 + l)
+          lo[l] = mid[l];
+        else
+          hi[l] = mid[l];
+      }
+    }
+    for (int l = 0; l < nl; ++l) {
+      const double sv = 0.5 * (lo[l] + hi[l]);
+      th[k - 1 - (j0 + l)] = sv * sv;
+    }
   }
   std::sort(th.begin(), th.end(), [](double a, double b) { return a > b; });
   for (int j = 0; j < k; ++j) theta[j] = th[j];
