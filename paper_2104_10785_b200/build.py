@@ -20,8 +20,7 @@ CSRC = HERE / "csrc"
 INCLUDE = ROOT / "include"
 LIB = HERE / "libksvd.so"
 SOURCES = [CSRC / "ksvd.cu", CSRC / "eig.cpp"]
-HEADERS = [CSRC / "kernels.cuh", CSRC / "gen.cuh", CSRC / "klrm.cuh", INCLUDE / "ksvd.h",
-           INCLUDE / "ksvd_gen.h"]
+HEADERS = sorted(CSRC.glob("*.cuh")) + [INCLUDE / "ksvd.h", INCLUDE / "ksvd_gen.h"]
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 
