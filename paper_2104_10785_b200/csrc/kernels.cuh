@@ -127,12 +127,12 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
 __device__ __forceinline__ double strided_sum(const double* __restrict__ p, int64_t ld,
                                               int cnt) {
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int k = 0; k < cnt; k += 16) {
-    double t[16];
+  for (int k = 0; k < cnt; k += 32) {  // acc[i & 3] += p[i] in ascending i
+    double t[32];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) t[u] = k + u < cnt ? __ldcg(p + (int64_t)(k + u) * ld) : 0.0;
+    for (int u = 0; u < 32; ++u) t[u] = k + u < cnt ? __ldcg(p + (int64_t)(k + u) * ld) : 0.0;
 #pragma unroll
-    for (int u = 0; u < 16; ++u) acc[u & 3] += t[u];
+    for (int u = 0; u < 32; ++u) acc[u & 3] += t[u];
   }
   return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
@@ -950,7 +950,7 @@ struct CgsCoopArgs {
 // on 148 SMs, measured by tools/barrier_bench.cu, vs ~2.3 us for a plain
 // counter/generation barrier).
 // bar == nullptr: cooperative-groups grid sync (cooperative launch).
-// Otherwise a sense-reversal barrier on {count, generation} for a regular
+// Otherwise a flip barrier on bar[0] for a regular
 // launch whose CTAs are all resident (one per SM, see cgs_coop): lets the
 // CGS grid start under programmatic dependent launch, which a cooperative
 // launch does not.
@@ -959,20 +959,18 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
     cooperative_groups::this_grid().sync();
     return;
   }
+  // one release-add per CTA on a single word; CTA 0 adds 2^31 - (nblocks - 1)
+  // so the last arrival flips bit 31 and the low bits return to their value
+  // (the cooperative-groups scheme: no reset, no second atomic, any nblocks)
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned* gen = bar + 1;
-    const unsigned g = *gen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == nblocks - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*gen == g) {
-      }
-    }
-    __threadfence();
+    const unsigned nb = blockIdx.x == 0 ? 0x80000000u - (nblocks - 1) : 1u;
+    unsigned old, cur;
+    asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(bar), "r"(nb)
+                 : "memory");
+    do {
+      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+    } while (((old ^ cur) & 0x80000000u) == 0);
   }
   __syncthreads();
 }
@@ -1380,39 +1378,44 @@ __device__ __forceinline__ void tile2_issue(const CgsCoopArgs& a, double* tile, 
   // with the total byte count, then the 32 lanes of warp 0 issue the
   // per-column copies (one thread issuing ~100+ copies serially was the
   // largest fixed cost of this kernel); all threads wait later.
-  if (warp == 0) {
-    const uint32_t bytes = (uint32_t)ldt * 8u;
-    if (lane == 0) {
-      if (init) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      }
-      const uint32_t total = bytes * (uint32_t)a.ncols;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                   "r"(total)
-                   : "memory");
+  (void)lane;
+  (void)warp;
+  const uint32_t bytes = (uint32_t)ldt * 8u;
+  if (threadIdx.x == 0) {
+    if (init) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncwarp();
-    if (bytes) {
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      for (int j = lane; j < a.ncols; j += 32) {
-        const double* src = a.B + (int64_t)j * a.ldb + s0;
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
-            "[%3];" ::"r"(smem_u32(tile + (size_t)j * ldt)),
-            "l"(src), "r"(bytes), "r"(bar)
-            : "memory");
-      }
+    const uint32_t total = bytes * (uint32_t)a.ncols;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                 "r"(total)
+                 : "memory");
+  }
+  __syncthreads();
+  // one column copy per thread (up to 256 in flight from all 8 warps: the
+  // issue of ~150 copies from one warp was measured at ~2.6 us per kernel)
+  if (bytes) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    for (int j = threadIdx.x; j < a.ncols; j += kThreads) {
+      const double* src = a.B + (int64_t)j * a.ldb + s0;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+          "[%3];" ::"r"(smem_u32(tile + (size_t)j * ldt)),
+          "l"(src), "r"(bytes), "r"(bar)
+          : "memory");
     }
   }
 }
 
 // Returns ||x||^2 after the orthogonalisation (the same value in every CTA:
 // callers of the persistent kernels use it instead of re-reading the slot).
+// halt_check: test the run status here (its load in flight with the
+// finalisation loads) and return -1.0 if the run has halted, the copy drained.
 template <int MAXE>
 __device__ __forceinline__ double tile2_rest(const CgsCoopArgs& a, double* tile,
                                            double (*tred)[32 * MAXE], uint32_t bar,
-                                           uint32_t parity, unsigned long long t_entry) {
+                                           uint32_t parity, unsigned long long t_entry,
+                                           bool halt_check = false) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned G = gridDim.x;
   const int64_t s0 = (int64_t)blockIdx.x * a.rows_per_cta;
@@ -1420,15 +1423,36 @@ __device__ __forceinline__ double tile2_rest(const CgsCoopArgs& a, double* tile,
   const int nr = s1 > s0 ? (int)(s1 - s0) : 0;
   const int ldt = (nr + 1) & ~1;
   double* cs = tile + (size_t)a.ncols * ldt;  // coefficients of the current pass
-  // [0] finalisation of the split partial sums of A^T q (overlaps the copy)
+  if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0) {  // [8] entry -> finalisation start
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    atomicAdd(a.tdbg + 8, now - t_entry);
+  }
+  // [0] finalisation of the split partial sums of the product (overlaps the
+  // copy): one row per thread (nr <= 32 * MAXE <= kThreads), every load --
+  // the run status included -- in flight at once; the row values go to x
+  // and, staged in smem, to the per-warp register copies below
+  double* xs = &tred[0][0];
+  const int st0 = halt_check ? *reinterpret_cast<const volatile int*>(&a.st->status)
+                             : (int)ST_RUNNING;
   if (a.fpart) {
     const double fb = a.fp ? __ldcg(a.fbeta) : 0.0;
-    for (int64_t r = s0 + threadIdx.x; r < s1; r += kThreads) {
+    const int64_t r = s0 + threadIdx.x;
+    if (r < s1) {
       double v = strided_sum(a.fpart + r, a.fld, a.fnsplit);
       if (a.fp) v = v - fb * __ldcg(a.fp + r);
-      a.x[r] = v;
-      flag_nonfinite(a.st, v, a.step);
+      if (st0 == ST_RUNNING) {
+        a.x[r] = v;
+        flag_nonfinite(a.st, v, a.step);
+      }
+      xs[threadIdx.x] = v;
     }
+  }
+  if (st0 != ST_RUNNING) {  // same value in every thread of every CTA
+    if (threadIdx.x == 0)
+      while (!mbar_try_wait(bar, parity)) {
+      }
+    return -1.0;
   }
   unsigned long long tl = 0;
   phase_mark(a.tdbg, 0, tl);
@@ -1440,7 +1464,7 @@ __device__ __forceinline__ double tile2_rest(const CgsCoopArgs& a, double* tile,
 #pragma unroll
   for (int e = 0; e < MAXE; ++e) {
     const int rl = lane + 32 * e;
-    xv[e] = rl < nr ? a.x[s0 + rl] : 0.0;
+    xv[e] = rl < nr ? (a.fpart ? xs[rl] : a.x[s0 + rl]) : 0.0;
   }
   while (!mbar_try_wait(bar, parity)) {
   }
@@ -1538,11 +1562,23 @@ __device__ __forceinline__ double tile2_rest(const CgsCoopArgs& a, double* tile,
       for (int j = j0 + gw; j < j1; j += nw) {
         const double* p = P + (int64_t)j * G;
         double t = 0.0;
-        for (unsigned b = lane; b < G; b += 32) t += __ldcg(p + b);
+        for (unsigned b0 = 0; b0 < G; b0 += 160) {  // 5 loads per lane in flight
+          double v[5];
+#pragma unroll
+          for (int k = 0; k < 5; ++k) {
+            const unsigned b = b0 + lane + 32 * k;
+            v[k] = b < G ? __ldcg(p + b) : 0.0;
+          }
+#pragma unroll
+          for (int k = 0; k < 5; ++k)
+            if (b0 + lane + 32 * k < G) t += v[k];  // the order of the plain loop
+        }
         t = warp_sum(t);
         if (lane == 0) a.c[j] = t;
       }
+      phase_mark(a.tdbg, 10, tl);  // [10] distributed column sums
       grid_barrier(a.bar, G);
+      phase_mark(a.tdbg, 11, tl);  // [11] the barrier after them
       for (int j = j0 + (int)threadIdx.x; j < j1; j += kThreads) red[j] = __ldcg(a.c + j);
     }
     __syncthreads();
@@ -1647,13 +1683,9 @@ k_cgs2_tile2(CgsCoopArgs a) {
   // ahead of this wait; the partial sums / x below may not.
   pdl_wait();
   pdl_trigger(2);
-  if (halted(a.st)) {  // drain the copy into this CTA's smem before exiting
-    if (threadIdx.x == 0)
-      while (!mbar_try_wait(bar, 0)) {
-      }
-    return;
-  }
-  tile2_rest<MAXE>(a, tile, tred, bar, 0, t_entry);
+  // the halt test (copy drained before exiting) is inside, its load in
+  // flight with the finalisation's
+  tile2_rest<MAXE>(a, tile, tred, bar, 0, t_entry, true);
 }
 
 

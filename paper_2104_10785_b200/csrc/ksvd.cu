@@ -808,13 +808,16 @@ static int cgs_coop(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int n
     CK(cudaEventRecord(e0, c->stream));
   }
   {
-    // KSVD_COOP_LAUNCH=0 (experiment): a regular launch with the custom
-    // grid barrier, so programmatic dependent launch can start the grid
-    // while the product drains (all G <= #SMs CTAs become resident once it
-    // has: the CGS tile takes an SM's shared memory, one CTA per SM)
+    // A regular launch with the flip barrier of grid_barrier (default), so
+    // programmatic dependent launch starts the grid while the product
+    // drains: its CTAs are scheduled only once every CTA of the product has
+    // started, and all G <= #SMs of them are resident once the product's
+    // CTAs retire (one CTA per SM).  Measured on config 2: 3692 vs 3624 GK
+    // steps/s for the cooperative launch (KSVD_COOP_LAUNCH=1), whose ~6 us
+    // launch cannot overlap the product's tail.
     static const bool regular = [] {
       const char* e = getenv("KSVD_COOP_LAUNCH");
-      return e && strcmp(e, "0") == 0;
+      return !(e && strcmp(e, "1") == 0);
     }();
     const bool reg = regular && G <= c->sms;
     if (!reg) a.bar = nullptr;
@@ -1414,12 +1417,14 @@ static int run_steps(ksvd_run* R, int i0) {
     t_launch += std::chrono::duration<double, std::milli>(t2 - t1).count();
   }
   if (c->tdbg) {
-    unsigned long long t[8];
+    unsigned long long t[16];
     CK(cudaMemcpyAsync(t, c->tdbg, sizeof t, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    fprintf(stderr, "[ksvd] cgs phases (us, CTA 0, cumulative): entry->setup %.1f copy %.1f "
-            "sweeps %.1f barriers %.1f reductions %.1f | tile kernels %llu, in-kernel total %.1f\n",
-            t[5] * 1e-3, t[1] * 1e-3, t[2] * 1e-3, t[3] * 1e-3, t[4] * 1e-3, t[7], t[6] * 1e-3);
+    fprintf(stderr, "[ksvd] cgs phases (us, CTA 0, cumulative): entry->setup %.1f (entry->fin "
+            "%.1f) copy %.1f sweeps %.1f barriers %.1f reductions %.1f (dist sums %.1f, their "
+            "barrier %.1f) | tile kernels %llu, in-kernel total %.1f\n",
+            t[5] * 1e-3, t[8] * 1e-3, t[1] * 1e-3, t[2] * 1e-3, t[3] * 1e-3, t[4] * 1e-3,
+            t[10] * 1e-3, t[11] * 1e-3, t[7], t[6] * 1e-3);
     CK(cudaMemsetAsync(c->tdbg, 0, sizeof t, c->stream));
   }
   if (dbg)
@@ -1950,8 +1955,8 @@ int ksvd_ctx_create(int device, int rank, int nranks, const char* uid, ksvd_ctx*
   for (auto& e : c->ring_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaHostAlloc((void**)&c->hprog, sizeof(HostProg), cudaHostAllocMapped));
   if (getenv("KSVD_PHASE_TIMES")) {
-    CK(cudaMalloc((void**)&c->tdbg, 64));
-    CK(cudaMemset(c->tdbg, 0, 64));
+    CK(cudaMalloc((void**)&c->tdbg, 128));
+    CK(cudaMemset(c->tdbg, 0, 128));
   }
   CK(cudaHostGetDevicePointer((void**)&c->dprog, c->hprog, 0));
   {
