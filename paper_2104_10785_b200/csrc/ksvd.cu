@@ -750,7 +750,14 @@ static int cgs_coop(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int n
   void* args[] = {&a};
 
   // tile-resident variant: one CTA per SM, each CTA's basis tile in smem
-  int64_t G = std::min<int64_t>(c->sms, std::max<int64_t>(1, cdiv(L, 32)));
+  // at least kCgsMinRows rows per CTA (KSVD_CGS_MINROWS overrides): fewer
+  // CTAs make the cross-CTA reductions and barriers cheaper, more rows per
+  // CTA make the shared-memory sweeps longer
+  static const int64_t min_rows = [] {
+    const char* e = getenv("KSVD_CGS_MINROWS");
+    return e ? std::max<int64_t>(2, atoll(e)) : (int64_t)32;
+  }();
+  int64_t G = std::min<int64_t>(c->sms, std::max<int64_t>(1, cdiv(L, min_rows)));
   int64_t rows = rup(cdiv(std::max<int64_t>(L, 1), G), 2);
   G = std::max<int64_t>(1, cdiv(L, rows));
   const size_t tile_bytes = sizeof(double) * (size_t)ncols * (size_t)(rows + 1);

@@ -194,8 +194,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_gk_resident(ResArgs a) {
         dots(basis, ld, ncols, x, len, partb(pp), pass + 1 == a.passes);
         continue;
       }
-      double cc = 0.0;
-      for (int j = 0; j < ncols; ++j) cc = fma(red[j], red[j], cc);
+      double cc = 0.0;  // same fixed order in every warp (lane strides + butterfly)
+      for (int j = (int)(threadIdx.x & 31); j < ncols; j += 32) cc = fma(red[j], red[j], cc);
+      cc = warp_sum(cc);
       const double nn = red[ncols];
       update(basis, ld, ncols, x, len);
       if (cc <= 1e-6 * nn) return nn - cc;
