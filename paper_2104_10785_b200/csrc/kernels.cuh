@@ -970,8 +970,25 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
     unsigned old, cur;
     asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(bar), "r"(nb)
                  : "memory");
+    // a regular launch relies on all nblocks CTAs becoming resident (one per
+    // SM, <= #SMs); should they not (an SM-limited MPS client or green
+    // context), fail loudly after ~20 s instead of spinning forever
+    // (KSVD_COOP_LAUNCH=1 selects the driver-checked cooperative launch)
+    unsigned polls = 0;
+    unsigned long long t0 = 0;
     do {
       asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+      if ((++polls & 0xfffu) == 0) {
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (t0 == 0) {
+          t0 = now;
+        } else if (now - t0 > 20000000000ull) {
+          printf("ksvd: grid barrier of %u CTAs timed out (not all CTAs resident?); "
+                 "KSVD_COOP_LAUNCH=1 selects the cooperative launch\n", nblocks);
+          __trap();
+        }
+      }
     } while (((old ^ cur) & 0x80000000u) == 0);
   }
   __syncthreads();

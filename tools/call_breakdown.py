@@ -1,4 +1,6 @@
-"""Host-side time breakdown of one estimate_rank call (config 2)."""
+"""Host-side time breakdown of one estimate_rank call (config 2): the GK
+loop (start vector, device loop, alpha/beta download), the rank path's
+bidiagonal SVD, the run release."""
 import sys
 import time
 from pathlib import Path
@@ -8,8 +10,7 @@ import numpy as np
 
 import paper_2104_10785_b200 as K
 from paper_2104_10785_b200 import _lib, synth
-from paper_2104_10785_b200.bidiag import run_gk
-from paper_2104_10785_b200.fsvd import _gram
+from paper_2104_10785_b200.bidiag import _start_vector, run_gk
 
 A = synth.config2_matrix(seed=1)
 op = K.DeviceMatrix.from_host(A)
@@ -18,10 +19,18 @@ ctx = _lib.get_context()
 for it in range(4):
     ctx.sync()
     t0 = time.perf_counter()
+    _start_vector(cfg, op.shape[0])
+    ts = time.perf_counter()
     run = run_gk(op, cfg)
     t1 = time.perf_counter()
-    theta, _ = K.symtridiag_eig(_gram(run.alphas, run.betas), vectors=False)
+    theta = _lib.bidiag_sv2(run.alphas, run.betas)
     t2 = time.perf_counter()
     run.free()
     t3 = time.perf_counter()
-    print(f"call {it}: run_gk {1e3*(t1-t0):.2f} ms, eig {1e3*(t2-t1):.2f} ms, free {1e3*(t3-t2):.2f} ms, k' {run.k_prime}")
+    print(f"call {it}: start vector {1e3*(ts-t0):.2f} ms, run_gk {1e3*(t1-ts):.2f} ms, "
+          f"bidiag_sv2 {1e3*(t2-t1):.2f} ms, free {1e3*(t3-t2):.2f} ms, k' {run.k_prime}")
+    ctx.sync()
+    t4 = time.perf_counter()
+    rep = K.estimate_rank(op, eps=1e-6, mode="relative", cfg=cfg)
+    ctx.sync()
+    print(f"        estimate_rank {1e3*(time.perf_counter()-t4):.2f} ms, rank {rep.rank}")
