@@ -946,6 +946,10 @@ struct CgsCoopArgs {
   const double* fp;
   unsigned long long* tdbg;  // nullable: phase timing of CTA 0
   int redundant;  // k_cgs2_tile2: every CTA reduces all partials (else distributed + barrier)
+  // regular launch, flag barrier: CTA b publishes epoch + k in flags[16 b]
+  // (its own 128-byte line) at its k-th barrier; nullptr: bar / cg sync
+  unsigned long long* flags;
+  unsigned long long epoch;
 };
 
 // Grid-wide barrier of the cooperative launch (cooperative_groups: ~1.2 us
@@ -956,7 +960,7 @@ struct CgsCoopArgs {
 // launch whose CTAs are all resident (one per SM, see cgs_coop): lets the
 // CGS grid start under programmatic dependent launch, which a cooperative
 // launch does not.
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
+__device__ __forceinline__ void grid_barrier_raw(unsigned* bar, unsigned nblocks) {
   if (bar == nullptr) {
     cooperative_groups::this_grid().sync();
     return;
@@ -992,6 +996,53 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
     } while (((old ^ cur) & 0x80000000u) == 0);
   }
   __syncthreads();
+}
+
+// Flag barrier (regular launch, G <= kThreads): no atomics -- CTA b stores
+// its target epoch to its own line, thread t of every CTA polls CTA t's line
+// (ld.acquire.gpu) until it reaches the target, so one release/acquire pair
+// per CTA pair replaces the serialised adds on one word.  Targets increase
+// across barriers and launches (host epoch + per-launch barrier count), so
+// the lines never need resetting.  Same bounded spin as grid_barrier_raw.
+__device__ __forceinline__ void flag_barrier(unsigned long long* flags, unsigned G,
+                                             unsigned long long target) {
+  __syncthreads();
+  if (threadIdx.x == 0)
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(flags + (size_t)blockIdx.x * 16),
+                 "l"(target)
+                 : "memory");
+  if (threadIdx.x < G) {
+    const unsigned long long* f = flags + (size_t)threadIdx.x * 16;
+    unsigned long long v;
+    unsigned polls = 0;
+    unsigned long long t0 = 0;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+      if ((++polls & 0xfffu) == 0) {
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (t0 == 0) {
+          t0 = now;
+        } else if (now - t0 > 20000000000ull) {
+          printf("ksvd: flag barrier of %u CTAs timed out (not all CTAs resident?); "
+                 "KSVD_COOP_LAUNCH=1 selects the cooperative launch\n", G);
+          __trap();
+        }
+      }
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+// the k-th grid-wide barrier of a CGS launch (k counted per thread: every
+// CTA passes the same sequence of barriers)
+__device__ __forceinline__ void grid_barrier(const CgsCoopArgs& a, unsigned G,
+                                             unsigned long long& k) {
+  ++k;
+  if (a.flags)
+    flag_barrier(a.flags, G, a.epoch + k);
+  else
+    grid_barrier_raw(a.bar, G);
 }
 
 // phase timestamps of CTA 0 (debug builds of the timing breakdown)
@@ -1032,6 +1083,7 @@ k_cgs2_coop(CgsCoopArgs a) {
   __shared__ double nacc;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned G = gridDim.x;
+  unsigned long long bk = 0;  // grid barriers passed in this launch
   const int64_t s0 = (int64_t)blockIdx.x * a.rows_per_cta;
   const int64_t s1 = min(a.L, s0 + a.rows_per_cta);
 
@@ -1129,13 +1181,13 @@ k_cgs2_coop(CgsCoopArgs a) {
   } else {
     sweep(false, true);
     for (int pass = 1; pass <= a.passes; ++pass) {
-      grid_barrier(a.bar, G);
+      grid_barrier(a, G, bk);
       coop_reduce_cols(a.part, a.ncols, (int)G, a.c);
-      grid_barrier(a.bar, G);
+      grid_barrier(a, G, bk);
       sweep(true, pass < a.passes);
     }
   }
-  grid_barrier(a.bar, G);
+  grid_barrier(a, G, bk);
   if (blockIdx.x == 0) {
     // [4] norm test (k_norm_test semantics, incl. the host progress word)
     double s = 0.0;
@@ -1189,6 +1241,7 @@ k_cgs2_tile(CgsCoopArgs a) {
   __shared__ double nacc;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned G = gridDim.x;
+  unsigned long long bk = 0;  // grid barriers passed in this launch
   const int64_t s0 = (int64_t)blockIdx.x * a.rows_per_cta;
   const int64_t s1 = min(a.L, s0 + a.rows_per_cta);
   const int nr = s1 > s0 ? (int)(s1 - s0) : 0;
@@ -1325,17 +1378,17 @@ k_cgs2_tile(CgsCoopArgs a) {
     sweep(false, true);
     phase_mark(a.tdbg, 2, tl);  // [2] sweeps
     for (int pass = 1; pass <= a.passes; ++pass) {
-      grid_barrier(a.bar, G);
+      grid_barrier(a, G, bk);
       phase_mark(a.tdbg, 3, tl);  // [3] barriers
       coop_reduce_cols(a.part, a.ncols, (int)G, a.c);
       phase_mark(a.tdbg, 4, tl);  // [4] reductions
-      grid_barrier(a.bar, G);
+      grid_barrier(a, G, bk);
       phase_mark(a.tdbg, 3, tl);
       sweep(true, pass < a.passes);
       phase_mark(a.tdbg, 2, tl);
     }
   }
-  grid_barrier(a.bar, G);
+  grid_barrier(a, G, bk);
   phase_mark(a.tdbg, 3, tl);
   if (blockIdx.x == 0) {
     double s = 0.0;
@@ -1437,6 +1490,7 @@ __device__ __forceinline__ double tile2_rest(const CgsCoopArgs& a, double* tile,
                                            bool halt_check = false) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned G = gridDim.x;
+  unsigned long long bk = 0;  // grid barriers passed in this launch
   const int64_t s0 = (int64_t)blockIdx.x * a.rows_per_cta;
   const int64_t s1 = min(a.L, s0 + a.rows_per_cta);
   const int nr = s1 > s0 ? (int)(s1 - s0) : 0;
@@ -1596,7 +1650,7 @@ __device__ __forceinline__ double tile2_rest(const CgsCoopArgs& a, double* tile,
         if (lane == 0) a.c[j] = t;
       }
       phase_mark(a.tdbg, 10, tl);  // [10] distributed column sums
-      grid_barrier(a.bar, G);
+      grid_barrier(a, G, bk);
       phase_mark(a.tdbg, 11, tl);  // [11] the barrier after them
       for (int j = j0 + (int)threadIdx.x; j < j1; j += kThreads) red[j] = __ldcg(a.c + j);
     }
@@ -1632,7 +1686,7 @@ __device__ __forceinline__ double tile2_rest(const CgsCoopArgs& a, double* tile,
 
   if (a.ncols == 0 || a.passes == 0) {
     dot(partb(0), true);
-    grid_barrier(a.bar, G);
+    grid_barrier(a, G, bk);
     reduce_all(partb(0), a.ncols, a.ncols + 1);
     finish(red[a.ncols]);
   } else {
@@ -1640,7 +1694,7 @@ __device__ __forceinline__ double tile2_rest(const CgsCoopArgs& a, double* tile,
     phase_mark(a.tdbg, 2, tl);
     for (int pass = 1; pass <= a.passes; ++pass) {
       const bool last = pass == a.passes;
-      grid_barrier(a.bar, G);
+      grid_barrier(a, G, bk);
       phase_mark(a.tdbg, 3, tl);
       reduce_all(partb(pass - 1), 0, a.ncols + (last ? 1 : 0));
       phase_mark(a.tdbg, 4, tl);
@@ -1674,7 +1728,7 @@ __device__ __forceinline__ double tile2_rest(const CgsCoopArgs& a, double* tile,
           s = warp_sum(s);
           if (lane == 0) partb(pass)[(int64_t)a.ncols * G + blockIdx.x] = s;
         }
-        grid_barrier(a.bar, G);
+        grid_barrier(a, G, bk);
         reduce_all(partb(pass), a.ncols, a.ncols + 1);
         finish(red[a.ncols]);
       }

@@ -581,6 +581,8 @@ struct CgsWork {
   double* c = nullptr;     // cap
   double* red = nullptr;   // 2
   unsigned* bar = nullptr; // grid barrier {count, generation}
+  unsigned long long* flags = nullptr;  // flag barrier: 256 lines of 128 bytes
+  unsigned long long epoch = 0;         // last target issued (16 per launch)
   int64_t part_elems = 0;
   int cap = 0;
 };
@@ -613,6 +615,10 @@ static int ensure_cgs(cudaStream_t s, CgsWork* w, int64_t nrb, int cols) {
   if (!w->bar) {
     CK(cudaMallocAsync((void**)&w->bar, sizeof(unsigned) * 2, s));
     CK(cudaMemsetAsync(w->bar, 0, sizeof(unsigned) * 2, s));
+  }
+  if (!w->flags) {
+    CK(cudaMallocAsync((void**)&w->flags, 256 * 128, s));
+    CK(cudaMemsetAsync(w->flags, 0, 256 * 128, s));
   }
   return 0;
 }
@@ -828,6 +834,19 @@ static int cgs_coop(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int n
     }();
     const bool reg = regular && G <= c->sms;
     if (!reg) a.bar = nullptr;
+    // KSVD_FLAG_BARRIER=1 (experiment): per-CTA flag lines polled by every
+    // CTA instead of the flip barrier's single word.  Measured on config 2:
+    // 3.8 vs 3.15 us of barrier time per CGS launch (the 148 x 148 polls
+    // contend in L2), 3698 vs 3733 GK steps/s -- so off by default.
+    static const bool flag_bar = [] {
+      const char* e = getenv("KSVD_FLAG_BARRIER");
+      return e && strcmp(e, "1") == 0;
+    }();
+    if (reg && flag_bar && G <= kThreads) {
+      a.flags = W->flags;
+      a.epoch = W->epoch;
+      W->epoch += 16;  // <= 5 barriers per CGS launch
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)G);
     cfg.blockDim = dim3(kThreads);
@@ -932,7 +951,8 @@ static void free_run(ksvd_run* R) {
                   (void*)R->beta, (void*)R->slot, (void*)R->G, (void*)R->V, (void*)R->U,
                   (void*)R->sig, (void*)R->left.part, (void*)R->left.c, (void*)R->left.red,
                   (void*)R->left.bar, (void*)R->right.part, (void*)R->right.c,
-                  (void*)R->right.red, (void*)R->right.bar, (void*)R->st, (void*)R->st_aux})
+                  (void*)R->right.red, (void*)R->right.bar, (void*)R->left.flags,
+                  (void*)R->right.flags, (void*)R->st, (void*)R->st_aux})
     if (p) cudaFreeAsync(p, c->stream);
   delete R;
 }

@@ -288,6 +288,7 @@ _MULTI = {"KSVD_RESIDENT": "0"}  # small cases would otherwise take the resident
                                  {"KSVD_PDL_TRIG": "3", **_MULTI}, {"KSVD_STREAM": "1", **_MULTI},
                                  {"KSVD_ROWS": "1", **_MULTI},
                                  {"KSVD_COOP_LAUNCH": "1", **_MULTI},
+                                 {"KSVD_FLAG_BARRIER": "1", **_MULTI},
                                  {"KSVD_COOP_LAUNCH": "1", "KSVD_CGS_SYNC": "5", **_MULTI},
                                  _MULTI, {}])
 def test_cgs_paths_agree(env):
