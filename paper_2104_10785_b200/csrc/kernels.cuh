@@ -49,6 +49,28 @@ struct HostProg {
   int pad;
 };
 
+// 1 when the host paces on the progress word (KSVD_PACE=spin); otherwise it
+// waits on events and reads only halt_step after them, so a breakdown needs
+// plain stores (visible once the kernel has completed) and the per-step
+// prog word -- a system-scope release store at the tail of every alpha-side
+// CGS kernel, on the step's critical path -- is not written at all.
+__constant__ int g_spin_pace = 0;
+
+// publish a norm test's outcome to the host (breakdowns always; in spin
+// mode also the step's last test, side 1, with a release store ordering
+// the status words before prog)
+__device__ __forceinline__ void host_progress(HostProg* hp, int stop, int step, int side) {
+  if (!hp) return;
+  if (stop != 0) {
+    volatile HostProg* h = hp;
+    h->status = stop;
+    h->halt_step = step;
+  }
+  if (g_spin_pace && (stop != 0 || side == 1))
+    asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(&hp->prog), "r"(2 * step + side)
+                 : "memory");
+}
+
 // Programmatic dependent launch (ksvd.cu launch_step): wait for the
 // preceding grid's completion + memory flush / let the next grid launch.
 // Every CTA of a kernel launched with the attribute calls pdl_wait() before
@@ -876,18 +898,7 @@ k_norm_test(const double* __restrict__ part, int nrb, const double* __restrict__
       st->kprime = step;
       st->where = step;
     }
-    // publish to the host: breakdowns always, otherwise only the step's last
-    // test (side 1); a release store orders the status words before prog
-    if (hp && (stop != ST_RUNNING || side == 1)) {
-      volatile HostProg* h = hp;
-      if (stop != ST_RUNNING) {
-        h->status = stop;
-        h->halt_step = step;
-      }
-      asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(&hp->prog),
-                   "r"(2 * step + side)
-                   : "memory");
-    }
+    host_progress(hp, stop, step, side);
   }
 }
 
@@ -1206,16 +1217,7 @@ k_cgs2_coop(CgsCoopArgs a) {
         a.st->kprime = a.step;
         a.st->where = a.step;
       }
-      if (a.hp && (stop != ST_RUNNING || a.side == 1)) {
-        volatile HostProg* h = a.hp;
-        if (stop != ST_RUNNING) {
-          h->status = stop;
-          h->halt_step = a.step;
-        }
-        asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(&a.hp->prog),
-                     "r"(2 * a.step + a.side)
-                     : "memory");
-      }
+      host_progress(a.hp, stop, a.step, a.side);
     }
   }
 }
@@ -1407,16 +1409,7 @@ k_cgs2_tile(CgsCoopArgs a) {
         a.st->kprime = a.step;
         a.st->where = a.step;
       }
-      if (a.hp && (stop != ST_RUNNING || a.side == 1)) {
-        volatile HostProg* h = a.hp;
-        if (stop != ST_RUNNING) {
-          h->status = stop;
-          h->halt_step = a.step;
-        }
-        asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(&a.hp->prog),
-                     "r"(2 * a.step + a.side)
-                     : "memory");
-      }
+      host_progress(a.hp, stop, a.step, a.side);
     }
   }
   if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1671,16 +1664,7 @@ __device__ __forceinline__ double tile2_rest(const CgsCoopArgs& a, double* tile,
         a.st->kprime = a.step;
         a.st->where = a.step;
       }
-      if (a.hp && (stop != ST_RUNNING || a.side == 1)) {
-        volatile HostProg* h = a.hp;
-        if (stop != ST_RUNNING) {
-          h->status = stop;
-          h->halt_step = a.step;
-        }
-        asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(&a.hp->prog),
-                     "r"(2 * a.step + a.side)
-                     : "memory");
-      }
+      host_progress(a.hp, stop, a.step, a.side);
     }
   };
 

@@ -1978,6 +1978,10 @@ int ksvd_ctx_create(int device, int rank, int nranks, const char* uid, ksvd_ctx*
     const int trig = atoi(e);
     CK(cudaMemcpyToSymbol(g_pdl_trig, &trig, sizeof trig));
   }
+  if (const char* e = getenv("KSVD_PACE")) {  // run_steps: progress-word pacing
+    const int spin = strcmp(e, "spin") == 0 ? 1 : 0;
+    CK(cudaMemcpyToSymbol(g_spin_pace, &spin, sizeof spin));
+  }
   for (auto& e : c->marks) CK(cudaEventCreate(&e));
   for (auto& e : c->ring_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaHostAlloc((void**)&c->hprog, sizeof(HostProg), cudaHostAllocMapped));

@@ -289,6 +289,7 @@ _MULTI = {"KSVD_RESIDENT": "0"}  # small cases would otherwise take the resident
                                  {"KSVD_ROWS": "1", **_MULTI},
                                  {"KSVD_COOP_LAUNCH": "1", **_MULTI},
                                  {"KSVD_FLAG_BARRIER": "1", **_MULTI},
+                                 {"KSVD_PACE": "spin", **_MULTI},
                                  {"KSVD_COOP_LAUNCH": "1", "KSVD_CGS_SYNC": "5", **_MULTI},
                                  _MULTI, {}])
 def test_cgs_paths_agree(env):
