@@ -260,7 +260,7 @@ def run_reference(args, rank, world):
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "effective_GBps": 2.0 * W["m"] * W["n"] * 8 * val / 1e9,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_ours(args, rank, world, dist):
@@ -444,10 +444,28 @@ def run_ours(args, rank, world, dist):
             "converged_top_k": converged,
             "clocks": clk.summary(),
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
+
+
+_JSON_OUT = None
+
+
+def emit(line):
+    """The one JSON line on the process's real stdout (see main)."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 
 def main():
+    global _JSON_OUT
+    # Library chatter (NCCL prints its version banner and warnings to fd 1
+    # when its debug level asks for it) must not precede the JSON line the
+    # driver parses: fd 1 is pointed at stderr for the whole run and the
+    # line goes to a duplicate of the original stdout.
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
