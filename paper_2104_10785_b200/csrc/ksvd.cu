@@ -456,7 +456,7 @@ static int launch_gemv_t(ksvd_mat* M, dim3 grid, const double* q_src, const doub
 static int dense_gemv_t(ksvd_mat* M, const double* q_src, const double* q_scale,
                         double* q_dst, const double* beta, const double* pprev,
                         double* z, DevState* st, int step, bool check,
-                        bool finalize = true) {
+                        bool finalize = true, bool axpy = true) {
   ksvd_ctx* c = M->ctx;
   const GemvTPlan& pt = M->pt;
   if (M->mloc > 0) {
@@ -491,7 +491,7 @@ static int dense_gemv_t(ksvd_mat* M, const double* q_src, const double* q_scale,
              (int)(check && !multi)));
   if (multi) {
     TRY(allreduce(c, z, (size_t)M->n_pad));
-    if (check || pprev)
+    if (axpy && (check || pprev))
       TRY(launch(c, KC_FIN, k_axpy_check, dim3((unsigned)cdiv(M->n, kThreads)),
                  dim3(kThreads), 0, z, beta, pprev, M->n, st, step));
   }
@@ -677,7 +677,7 @@ constexpr size_t kTileSmemMax = 200 * 1024;  // basis tile budget of k_cgs2_tile
 // with ~L/128 CTAs streams the basis faster than a one-wave cooperative grid
 // (measured: config 3 581 vs 600 ms per call).  KSVD_COOP=0 disables the
 // fused path, KSVD_COOP_GLOBAL=1 also uses the streaming cooperative kernel.
-static bool coop_enabled(const ksvd_ctx* c, int64_t L, int ncols) {
+static bool coop_enabled(const ksvd_ctx* c, int64_t L, int ncols, bool sharded) {
   static const bool off = [] {
     const char* e = getenv("KSVD_COOP");
     return e && strcmp(e, "0") == 0;
@@ -686,7 +686,9 @@ static bool coop_enabled(const ksvd_ctx* c, int64_t L, int ncols) {
     const char* e = getenv("KSVD_COOP_GLOBAL");
     return e && strcmp(e, "1") == 0;
   }();
-  if (off || c->comm != nullptr || ncols > kCoopMaxCols) return false;
+  // a sharded basis needs all-reduces between the passes (multi-kernel path);
+  // the replicated right basis takes the fused kernel at any rank count
+  if (off || (sharded && c->comm != nullptr) || ncols > kCoopMaxCols) return false;
   const int64_t G = std::min<int64_t>(c->sms, std::max<int64_t>(1, cdiv(L, 32)));
   const int64_t rows = rup(cdiv(std::max<int64_t>(L, 1), G), 2);
   const bool tile =
@@ -984,11 +986,11 @@ static int enqueue_step(ksvd_run* R, int i) {
   {
     SecTimer t(1);
     TRY(enqueue_gemv_n(M, R->z, R->alpha + i, Pcol(R, i - 1), Qcol(R, i - 1), R->alpha + i,
-                       R->w, R->st, i, /*finalize=*/!coop_enabled(c, M->mloc, i)));
+                       R->w, R->st, i, /*finalize=*/!coop_enabled(c, M->mloc, i, true)));
   }
   SecTimer t_cgs(2);
   // CGS2 against Q[:, :i]; beta_{i+1} = ||w||; beta < eps -> breakdown
-  if (coop_enabled(c, M->mloc, i)) {
+  if (coop_enabled(c, M->mloc, i, true)) {
     const FinArgs fin = fin_left(M, R->alpha + i, Qcol(R, i - 1));
     TRY(cgs_coop(c, &R->left, R->Q, R->ldq, i, R->w, M->mloc, R->reorth, R->eps,
                  R->beta + i + 1, R->st, i, ST_BETA_BREAK, R->M->ctx->dprog, 0, fin));
@@ -1005,10 +1007,22 @@ static int enqueue_step(ksvd_run* R, int i) {
   }
   // z = A^T q_{i+1} - beta_{i+1} p_i, q_{i+1} = w / beta stored to Q[:, i];
   // then CGS2 against P[:, :i] (replicated, no collective); alpha_{i+1} = ||z||
-  if (coop_enabled(c, M->n, i)) {
-    TRY(enqueue_gemv_t(M, R->w, R->beta + i + 1, Qcol(R, i), R->beta + i + 1, Pcol(R, i - 1),
-                       R->z, R->st, i, true, /*finalize=*/false));
-    const FinArgs fin = fin_right(M, R->beta + i + 1, Pcol(R, i - 1));
+  if (coop_enabled(c, M->n, i, false)) {
+    FinArgs fin;
+    if (c->comm != nullptr && !M->fac) {
+      // multi-rank dense A: z = all-reduce of the split sums first; the CGS
+      // kernel's finalisation applies - beta p and the non-finite check
+      // (the peer-exchange epilogue kernel already did both)
+      TRY(dense_gemv_t(M, R->w, R->beta + i + 1, Qcol(R, i), R->beta + i + 1,
+                       Pcol(R, i - 1), R->z, R->st, i, true, /*finalize=*/true,
+                       /*axpy=*/false));
+      if (!(c->px && M->n_pad <= c->px_slot))
+        fin = FinArgs{R->z, M->n_pad, 1, R->beta + i + 1, Pcol(R, i - 1)};
+    } else {
+      TRY(enqueue_gemv_t(M, R->w, R->beta + i + 1, Qcol(R, i), R->beta + i + 1,
+                         Pcol(R, i - 1), R->z, R->st, i, true, /*finalize=*/false));
+      fin = fin_right(M, R->beta + i + 1, Pcol(R, i - 1));
+    }
     TRY(cgs_coop(c, &R->right, R->P, R->ldp, i, R->z, M->n, R->reorth, R->eps,
                  R->alpha + i + 1, R->st, i, ST_ALPHA_BREAK, R->M->ctx->dprog, 1, fin));
   } else {
