@@ -1750,6 +1750,161 @@ k_cgs2_tile2(CgsCoopArgs a) {
 }
 
 
+// Multi-rank CGS2 of a row-sharded basis with the tile in shared memory:
+// the passes of k_cgs2_tile2 as three launches, the host's all-reduces of
+// the coefficient vector between them (the multi-kernel path needs eight
+// launches for the same CGS2):
+//   phase 0: finalisation of k_gemv_n2's chunk partials (x = A p - alpha q),
+//            partial B^T x -> grid barrier -> distributed column sums -> c
+//   phase 1: x -= B c (c all-reduced by the host) ; partial B^T x -> ... -> c
+//   phase 2: x -= B c ; ||x||^2 of this rank's rows (CTA 0, fixed order) and
+//            the local non-finite flag -> c[0], c[1] (all-reduced by the host
+//            and tested by k_norm_test, so every rank halts at the same step)
+// The same shared-memory sweeps and fixed-order sums as k_cgs2_tile2.
+template <int MAXE>
+__global__ void __launch_bounds__(kThreads, 1)
+k_cgs_tile_phase(CgsCoopArgs a, int phase) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ double tred[kWarps][32 * MAXE];
+  __shared__ double red8[kWarps];
+  __shared__ __align__(8) unsigned long long mbar;
+  double* tile = reinterpret_cast<double*>(smem_raw);
+  const uint32_t bar = smem_u32(&mbar);
+  tile2_issue(a, tile, bar, true);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned G = gridDim.x;
+  unsigned long long bk = 0;
+  const int64_t s0 = (int64_t)blockIdx.x * a.rows_per_cta;
+  const int64_t s1 = min(a.L, s0 + a.rows_per_cta);
+  const int nr = s1 > s0 ? (int)(s1 - s0) : 0;
+  const int ldt = (nr + 1) & ~1;
+  double* red = tile + (size_t)a.ncols * ldt;  // the reduced coefficients
+  double* xs = &tred[0][0];
+  // x rows (finalised from the product partials in phase 0), the all-reduced
+  // coefficients and the run status, all loads in flight together
+  const int st0 = *reinterpret_cast<const volatile int*>(&a.st->status);
+  if (phase == 0 && a.fpart) {
+    const double fb = a.fp ? __ldcg(a.fbeta) : 0.0;
+    const int64_t r = s0 + threadIdx.x;
+    if (r < s1) {
+      double v = strided_sum(a.fpart + r, a.fld, a.fnsplit);
+      if (a.fp) v = v - fb * __ldcg(a.fp + r);
+      if (st0 == ST_RUNNING) {
+        a.x[r] = v;
+        flag_nonfinite(a.st, v, a.step);
+      }
+      xs[threadIdx.x] = v;
+    }
+  } else if (threadIdx.x < nr) {
+    xs[threadIdx.x] = __ldcg(a.x + s0 + threadIdx.x);
+  }
+  if (phase > 0)
+    for (int j = threadIdx.x; j < a.ncols; j += kThreads) red[j] = __ldcg(a.c + j);
+  if (st0 != ST_RUNNING) {
+    if (threadIdx.x == 0)
+      while (!mbar_try_wait(bar, 0)) {
+      }
+    return;
+  }
+  __syncthreads();
+  double xv[MAXE];
+#pragma unroll
+  for (int e = 0; e < MAXE; ++e) {
+    const int rl = lane + 32 * e;
+    xv[e] = rl < nr ? xs[rl] : 0.0;
+  }
+  while (!mbar_try_wait(bar, 0)) {
+  }
+  __syncthreads();  // xs (tred) is reused below
+  if (phase > 0) {  // xv -= tile * red; store x
+    double t[MAXE];
+#pragma unroll
+    for (int e = 0; e < MAXE; ++e) t[e] = 0.0;
+#pragma unroll 4
+    for (int j = warp; j < a.ncols; j += kWarps) {
+      const double cj = red[j];
+      const double* col = tile + (size_t)j * ldt;
+#pragma unroll
+      for (int e = 0; e < MAXE; ++e) {
+        const int rl = lane + 32 * e;
+        if (rl < nr) t[e] = fma(col[rl], cj, t[e]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < MAXE; ++e) tred[warp][lane + 32 * e] = t[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < MAXE; ++e) {
+      double sum = tred[0][lane + 32 * e];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) sum += tred[w][lane + 32 * e];
+      xv[e] = xv[e] - sum;
+      const int rl = lane + 32 * e;
+      if (warp == 0 && rl < nr) a.x[s0 + rl] = xv[e];
+    }
+  }
+  if (phase < 2) {
+    // partial dots of this CTA -> part[j*G + b]
+    for (int q0 = 0; warp + kWarps * q0 < a.ncols; q0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = warp + kWarps * (q0 + u);
+        v[u] = 0.0;
+        if (j < a.ncols) {
+          const double* col = tile + (size_t)j * ldt;
+#pragma unroll
+          for (int e = 0; e < MAXE; ++e) {
+            const int rl = lane + 32 * e;
+            if (rl < nr) v[u] = fma(col[rl], xv[e], v[u]);
+          }
+        }
+      }
+      const double t = warp_sum8(v);
+      const int j = warp + kWarps * (q0 + warp_sum8_index(lane));
+      if ((lane & 3) == 0 && j < a.ncols) a.part[(int64_t)j * G + blockIdx.x] = t;
+    }
+    grid_barrier(a, G, bk);
+    // c[j] = sum_b part[j*G + b]: the grid's warps take columns round-robin
+    const int gw = blockIdx.x * kWarps + warp, nw = (int)G * kWarps;
+    for (int j = gw; j < a.ncols; j += nw) {
+      const double* p = a.part + (int64_t)j * G;
+      double t = 0.0;
+      for (unsigned b0 = 0; b0 < G; b0 += 160) {
+        double v[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const unsigned b = b0 + lane + 32 * k;
+          v[k] = b < G ? __ldcg(p + b) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 5; ++k)
+          if (b0 + lane + 32 * k < G) t += v[k];
+      }
+      t = warp_sum(t);
+      if (lane == 0) a.c[j] = t;
+    }
+  } else {
+    if (warp == kWarps - 1) {
+      double sq = 0.0;
+#pragma unroll
+      for (int e = 0; e < MAXE; ++e) sq = fma(xv[e], xv[e], sq);
+      sq = warp_sum(sq);
+      if (lane == 0) a.part[blockIdx.x] = sq;
+    }
+    grid_barrier(a, G, bk);
+    if (blockIdx.x == 0) {
+      double sq = 0.0;
+      for (unsigned b = threadIdx.x; b < G; b += kThreads) sq += __ldcg(a.part + b);
+      sq = block_sum(sq, red8);
+      if (threadIdx.x == 0) {
+        a.c[0] = sq;
+        a.c[1] = *reinterpret_cast<volatile int*>(&a.st->nonfinite) ? 1.0 : 0.0;
+      }
+    }
+  }
+}
+
 // dst = src / val (host scalar; terminal column, bidiag.py:101)
 __global__ void __launch_bounds__(kThreads)
 k_scale_val(const double* __restrict__ src, double val, double* __restrict__ dst,

@@ -897,6 +897,107 @@ static int cgs(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int ncols,
   }
 }
 
+// ---- multi-rank CGS2 of a row-sharded basis, tile in shared memory ----
+// k_cgs_tile_phase: 3 launches (2 with one pass) and k_norm_test around the
+// 3 all-reduces, instead of the multi-kernel path's 8 launches.  Applies when
+// this rank's rows give <= 256 rows per CTA and the tile fits shared memory
+// (KSVD_MTILE=0 keeps the multi-kernel path).
+struct TileGeom {
+  int64_t G = 0, rows = 0;
+  size_t smem = 0;
+  bool ok = false;
+};
+static TileGeom tile_geom(const ksvd_ctx* c, int64_t L, int ncols) {
+  TileGeom g;
+  g.G = std::min<int64_t>(c->sms, std::max<int64_t>(1, cdiv(L, 32)));
+  g.rows = rup(cdiv(std::max<int64_t>(L, 1), g.G), 2);
+  g.G = std::max<int64_t>(1, cdiv(L, g.rows));
+  const size_t tile_bytes = sizeof(double) * (size_t)ncols * (size_t)(g.rows + 1);
+  g.smem = tile_bytes + 16;
+  g.ok = L > 0 && ncols > 0 && g.rows <= 256 && g.smem <= kTileSmemMax;
+  return g;
+}
+static bool multi_tile_enabled(const ksvd_ctx* c, int64_t L, int ncols) {
+  static const bool off = [] {
+    const char* e = getenv("KSVD_MTILE");
+    return e && strcmp(e, "0") == 0;
+  }();
+  return !off && c->comm != nullptr && tile_geom(c, L, ncols).ok;
+}
+
+template <int E>
+static const void* phase_kernel() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(k_cgs_tile_phase<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kTileSmemMax);
+    done = true;
+  }
+  return (const void*)k_cgs_tile_phase<E>;
+}
+
+static int cgs_tile_multi(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int ncols,
+                          double* x, int64_t L, int passes, double eps, double* slot,
+                          DevState* st, int step, int code, HostProg* hp, int side,
+                          const FinArgs& fin) {
+  const TileGeom g = tile_geom(c, L, ncols);
+  const void* kern = nullptr;
+  switch ((int)cdiv(g.rows, 32)) {
+    case 1: kern = phase_kernel<1>(); break;
+    case 2: kern = phase_kernel<2>(); break;
+    case 3: kern = phase_kernel<3>(); break;
+    case 4: kern = phase_kernel<4>(); break;
+    case 5: kern = phase_kernel<5>(); break;
+    case 6: kern = phase_kernel<6>(); break;
+    case 7: kern = phase_kernel<7>(); break;
+    default: kern = phase_kernel<8>(); break;
+  }
+  TRY(ensure_cgs(c->stream, W, g.G, 2 * (ncols + 1)));
+  CgsCoopArgs a{};
+  a.B = B;
+  a.ldb = ldb;
+  a.ncols = ncols;
+  a.x = x;
+  a.L = L;
+  a.rows_per_cta = (int)g.rows;
+  a.st = st;
+  a.step = step;
+  a.part = W->part;
+  a.c = W->c;
+  a.bar = W->bar;  // regular launch, flip barrier (one CTA per SM, G <= #SMs)
+  a.tdbg = nullptr;
+  const int phases[3] = {0, 1, 2};
+  for (int k = 0; k < 3; ++k) {
+    int phase = phases[k];
+    if (phase == 1 && passes < 2) continue;
+    if (phase == 0) {
+      a.fpart = fin.part;
+      a.fld = fin.ld;
+      a.fnsplit = fin.nsplit;
+      a.fbeta = fin.beta;
+      a.fp = fin.p;
+    } else {
+      a.fpart = nullptr;
+    }
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->profiling) {
+      TRY(get_event(c, &e0));
+      TRY(get_event(c, &e1));
+      CK(cudaEventRecord(e0, c->stream));
+    }
+    void* args[] = {&a, &phase};
+    CK(cudaLaunchKernel(kern, dim3((unsigned)g.G), dim3(kThreads), args, g.smem, c->stream));
+    if (c->profiling) {
+      CK(cudaEventRecord(e1, c->stream));
+      c->pending.push_back({e0, e1, KC_CGS});
+    }
+    c->launches++;
+    TRY(allreduce(c, W->c, phase < 2 ? (size_t)ncols : 2));
+  }
+  return launch(c, KC_CGS, k_norm_test, dim3(1), dim3(kThreads), 0, (const double*)nullptr, 0,
+                (const double*)W->c, eps, slot, st, step, code, hp, side);
+}
+
 // ---------------------------------------------------------------------------
 // runs
 constexpr int kLag = 3;   // steps enqueued ahead of the last completed one
@@ -986,11 +1087,17 @@ static int enqueue_step(ksvd_run* R, int i) {
   {
     SecTimer t(1);
     TRY(enqueue_gemv_n(M, R->z, R->alpha + i, Pcol(R, i - 1), Qcol(R, i - 1), R->alpha + i,
-                       R->w, R->st, i, /*finalize=*/!coop_enabled(c, M->mloc, i, true)));
+                       R->w, R->st, i,
+                       /*finalize=*/!coop_enabled(c, M->mloc, i, true) &&
+                           !multi_tile_enabled(c, M->mloc, i)));
   }
   SecTimer t_cgs(2);
   // CGS2 against Q[:, :i]; beta_{i+1} = ||w||; beta < eps -> breakdown
-  if (coop_enabled(c, M->mloc, i, true)) {
+  if (multi_tile_enabled(c, M->mloc, i)) {
+    const FinArgs fin = fin_left(M, R->alpha + i, Qcol(R, i - 1));
+    TRY(cgs_tile_multi(c, &R->left, R->Q, R->ldq, i, R->w, M->mloc, R->reorth, R->eps,
+                       R->beta + i + 1, R->st, i, ST_BETA_BREAK, R->M->ctx->dprog, 0, fin));
+  } else if (coop_enabled(c, M->mloc, i, true)) {
     const FinArgs fin = fin_left(M, R->alpha + i, Qcol(R, i - 1));
     TRY(cgs_coop(c, &R->left, R->Q, R->ldq, i, R->w, M->mloc, R->reorth, R->eps,
                  R->beta + i + 1, R->st, i, ST_BETA_BREAK, R->M->ctx->dprog, 0, fin));
