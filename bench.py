@@ -49,7 +49,6 @@ METRIC = ("GK steps/s & time to top-k SVD; A·v+Aᵀu HBM GB/s vs roofline "
           "at 1/2/4/8 GPU")
 UNIT = "GK steps/s"
 FALLBACK_HBM_GBS = 6650.0
-REF_SAMPLE_STEPS = 48   # GK iterations per reference-arm step (host configs)
 REF_SAMPLE_ROWS = 8192  # rows of the CPU sample for device-generated configs
 
 
@@ -198,12 +197,15 @@ def cpu_sample(W, A_host=None):
             O.fsvd_oracle(A, W["k"], W["r"], eps=W["eps"], seed=W["seed"])
             dt = time.perf_counter() - t0
             return W["k"] / dt, "one full oracle fsvd call on the config matrix", dt
+        # the whole reference call (GK loop to breakdown + the Gram eigenvalues
+        # + the count): ~3 s on 16 host cores for config 2; a loop truncated
+        # early would omit the CGS2 cost that grows with the step
         t0 = time.perf_counter()
-        g = O.gk_oracle(A, min(REF_SAMPLE_STEPS, min(A.shape)), eps=1e-8, seed=W["seed"])
+        rep = O.rank_oracle(A, eps=W["eps"], mode=W["mode"], seed=W["seed"])
         dt = time.perf_counter() - t0
-        return (g.k_prime / dt,
-                f"oracle GK loop truncated at {REF_SAMPLE_STEPS} iterations on the config matrix",
-                dt)
+        return (rep.k_prime / dt,
+                "one full oracle estimate_rank call on the config matrix "
+                f"(k' {rep.k_prime}, rank {rep.rank})", dt)
     # device-generated configs: a host sample of the same width, rate
     # extrapolated by bytes (the CPU products are bandwidth-bound)
     rows = min(REF_SAMPLE_ROWS, W["m"])
