@@ -1770,7 +1770,10 @@ k_cgs_tile_phase(CgsCoopArgs a, int phase) {
   __shared__ __align__(8) unsigned long long mbar;
   double* tile = reinterpret_cast<double*>(smem_raw);
   const uint32_t bar = smem_u32(&mbar);
+  // the basis columns were written >= 2 launches back: the tile copy may
+  // run ahead of the programmatic-launch wait, nothing else may
   tile2_issue(a, tile, bar, true);
+  pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned G = gridDim.x;
   unsigned long long bk = 0;

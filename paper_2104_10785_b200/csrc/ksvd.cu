@@ -137,17 +137,25 @@ static int collect_profile(ksvd_ctx* c) {
   return 0;
 }
 
-// Programmatic dependent launch for the GK step kernels (single rank): the
-// next kernel's CTAs are scheduled while the current one drains and run
-// their prologue (k_cgs2_tile: the TMA load of the basis tile) before
+// Programmatic dependent launch for the GK step kernels: the next kernel's
+// CTAs are scheduled while the current one drains and run their prologue
+// (k_cgs2_tile2 / k_cgs_tile_phase: the TMA load of the basis tile) before
 // griddepcontrol.wait.  Every kernel launched this way calls pdl_wait() in
 // every CTA before touching its predecessor's outputs (kernels.cuh).
+// Multi-rank: only our own step kernels carry the attribute; the kernels
+// that trigger early (k_gemv_n2, k_gemv_t2) are always followed by one of
+// ours, never directly by a collective, so an NCCL kernel never starts
+// before its input is complete (KSVD_PDL_MULTI=0 disables PDL there).
 static bool pdl_enabled(const ksvd_ctx* c) {
   static const bool off = [] {
     const char* e = getenv("KSVD_PDL");
     return e && strcmp(e, "0") == 0;
   }();
-  return !off && c->comm == nullptr;
+  static const bool multi_off = [] {
+    const char* e = getenv("KSVD_PDL_MULTI");
+    return e && strcmp(e, "0") == 0;
+  }();
+  return !off && (c->comm == nullptr || !multi_off);
 }
 
 template <typename... KArgs, typename... Args>
@@ -986,7 +994,17 @@ static int cgs_tile_multi(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb,
       CK(cudaEventRecord(e0, c->stream));
     }
     void* args[] = {&a, &phase};
-    CK(cudaLaunchKernel(kern, dim3((unsigned)g.G), dim3(kThreads), args, g.smem, c->stream));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)g.G);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = g.smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled(c) ? 1 : 0;
+    CK(cudaLaunchKernelExC(&cfg, kern, args));
     if (c->profiling) {
       CK(cudaEventRecord(e1, c->stream));
       c->pending.push_back({e0, e1, KC_CGS});

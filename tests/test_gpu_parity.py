@@ -284,6 +284,7 @@ _MULTI = {"KSVD_RESIDENT": "0"}  # small cases would otherwise take the resident
                                  {"KSVD_FORCE_NCCL": "1"}, {"KSVD_FORCE_PX": "1"},
                                  {"KSVD_FORCE_NCCL": "1", "KSVD_MTILE": "0"},
                                  {"KSVD_FORCE_PX": "1", "KSVD_MTILE": "0"},
+                                 {"KSVD_FORCE_NCCL": "1", "KSVD_PDL_MULTI": "0"},
                                  {"KSVD_COOP_GLOBAL": "1", "KSVD_TILE": "0", **_MULTI},
                                  {"KSVD_CGS_SYNC": "5", **_MULTI}, {"KSVD_RED_MAX": "0", **_MULTI},
                                  {"KSVD_RED_MAX": "100000000", **_MULTI}, {"KSVD_PDL": "0", **_MULTI},
