@@ -83,6 +83,11 @@ int ksvd_ctx_create(int device, int rank, int nranks, const char *uid,
                     ksvd_ctx **out);
 int ksvd_ctx_destroy(ksvd_ctx *ctx);
 int ksvd_ctx_sync(ksvd_ctx *ctx);
+/* Synchronise and return the device's freed stream-ordered pool memory to
+ * the system (matrices and runs are pool allocations, kept mapped between
+ * calls so the GK loop never unmaps; after freeing a large matrix this
+ * makes the memory available to other allocators). */
+int ksvd_ctx_release_pool(ksvd_ctx *ctx);
 /* Per-kernel-class device timing (CUDA events on the launching stream). */
 int ksvd_ctx_set_profiling(ksvd_ctx *ctx, int on);
 /* cls: 0 gemv_n (A p), 1 gemv_t (A^T q), 2 CGS2 + norms, 3 other,

@@ -51,6 +51,7 @@ SIGNATURES = {
     "ksvd_ctx_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(_vp)]),
     "ksvd_ctx_destroy": (C.c_int, [_vp]),
     "ksvd_ctx_sync": (C.c_int, [_vp]),
+    "ksvd_ctx_release_pool": (C.c_int, [_vp]),
     "ksvd_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "ksvd_ctx_kernel_stats": (C.c_int, [_vp, C.c_int, _pi64, _pd]),
     "ksvd_ctx_reset_stats": (C.c_int, [_vp]),
@@ -151,6 +152,10 @@ class Context:
 
     def sync(self):
         check(load_library().ksvd_ctx_sync(self.handle))
+
+    def release_pool(self):
+        """Return freed device pool memory (e.g. after freeing a large matrix)."""
+        check(load_library().ksvd_ctx_release_pool(self.handle))
 
     # ---- measurement hooks (bench.py) ----
     def set_profiling(self, on: bool):

@@ -2284,6 +2284,15 @@ int ksvd_ctx_sync(ksvd_ctx* c) {
   return 0;
 }
 
+int ksvd_ctx_release_pool(ksvd_ctx* c) {
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  cudaMemPool_t pool;
+  CK(cudaDeviceGetDefaultMemPool(&pool, c->device));
+  CK(cudaMemPoolTrimTo(pool, 0));
+  return 0;
+}
+
 int ksvd_ctx_set_profiling(ksvd_ctx* c, int on) {
   TRY(collect_profile(c));
   c->profiling = on != 0;

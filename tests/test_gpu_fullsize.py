@@ -14,8 +14,9 @@ checked against the oracle in test_gpu_generator.py):
 * estimate_rank: the planted rank exactly (config 5: r = 300, s_300 = 1e-3
   far above the 1e-8 relative threshold, the 1e-12 noise far below it).
 
-Ordered largest first: the stream-ordered pool keeps freed blocks mapped,
-and the later (smaller) matrices reuse config 4's block.
+Ordered largest first, and each test returns its matrix's pool memory
+(ksvd_ctx_release_pool): the stream-ordered pool keeps freed blocks mapped,
+which would otherwise leave the later tests (and torch's allocator) ~20 GB.
 """
 
 import gc
@@ -25,7 +26,7 @@ import numpy as np
 import pytest
 
 import paper_2104_10785_b200 as K
-from paper_2104_10785_b200 import synth
+from paper_2104_10785_b200 import _lib, synth
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -73,6 +74,7 @@ def check_fsvd(cfg, rtol_res):
         op.free()
         del op
         gc.collect()
+        _lib.get_context().release_pool()  # the next tests get the HBM back
 
 
 def test_config4_fsvd_full_size():
@@ -106,8 +108,19 @@ def test_config5_rank_full_size():
         op.free()
         del op
         gc.collect()
+        _lib.get_context().release_pool()  # the next tests get the HBM back
 
 
 def test_config3_fsvd_full_size():
     """2e5 x 2e4 f64 (32 GB): converged top 20 of the harmonic spectrum."""
     check_fsvd(3, 1e-10)
+
+
+def test_pool_released():
+    """After the full-size matrices are freed and the pool trimmed, the HBM
+    is available to other allocators again."""
+    import torch
+
+    free, total = torch.cuda.mem_get_info()
+    print(f"free after release: {free / 1e9:.1f} of {total / 1e9:.1f} GB")
+    assert free > 0.8 * total
