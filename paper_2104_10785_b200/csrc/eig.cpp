@@ -279,7 +279,10 @@ extern "C" int ksvd_bidiag_sv2(int k, const double* alphas, const double* betas,
 // T, U, V column-major k x k; s descending; sign of each column pair fixed so
 // that U[:, j] = T V[:, j] / s_j (U columns of zero singular values are left
 // as the normalised zero column, i.e. 0).
-extern "C" int ksvd_dense_svd(int k, const double* T, double* U, double* s, double* V) {
+// AVX2 clone picked at load time where the host has it (the rotations and
+// column dots vectorise 4-wide; same operation order, identical results)
+extern "C" __attribute__((target_clones("avx2", "default"))) int ksvd_dense_svd(
+    int k, const double* T, double* U, double* s, double* V) {
   if (k <= 0) return ksvd_set_error_from_host(KSVD_ECONFIG, "empty matrix");
   const size_t K = (size_t)k;
   std::vector<double> W(T, T + K * K), Vm(K * K, 0.0);
