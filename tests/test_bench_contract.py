@@ -40,3 +40,26 @@ def test_reference_arm_line():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
     assert "workload" in line["config"]
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(900)
+def test_bench_stdout_is_one_json_line_with_nccl():
+    """Our arm through the multi-rank code path (NCCL initialised, which prints
+    its version banner to fd 1 on some boxes): stdout must still be exactly
+    the one JSON line the driver parses, with every key it reads."""
+    import os
+
+    env = {**os.environ, "KSVD_FORCE_NCCL": "1", "NCCL_DEBUG": "VERSION"}
+    res = subprocess.run([sys.executable, "bench.py", "--config", "1", "--steps", "1",
+                          "--warmup", "1", "--no-cpu-baseline"], cwd=ROOT, env=env,
+                         capture_output=True, text=True, timeout=800)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = res.stdout.strip().splitlines()
+    assert len(lines) == 1, res.stdout[:2000]
+    line = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+                "roofline", "e2e", "gpu_launches", "clocks"):
+        assert key in line, key
+    assert line["value"] > 0 and line["gpu_launches"] > 0
