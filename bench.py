@@ -114,6 +114,50 @@ def call(K, W, A):
     return rep.k_prime, 8 * (2 * rep.k_prime + 1)
 
 
+def stage_breakdown(K, W, op, ctx):
+    """One call of the entry point split into its stages, each timed on the
+    host with a device sync after it (every rank runs it: the GK loop is
+    collective); the same pieces fsvd / estimate_rank chain."""
+    import ctypes as C
+
+    from paper_2104_10785_b200 import _lib
+    from paper_2104_10785_b200.bidiag import run_gk
+    from paper_2104_10785_b200.fsvd import _gram, symtridiag_eig
+
+    if W["kind"] == "fsvd":
+        cfg = K.BidiagConfig(k_max=W["k"], eps=W["eps"], seed=W["seed"])
+    else:
+        cfg = K.BidiagConfig(k_max=min(W["m"], W["n"]), seed=W["seed"])
+    ctx.sync()
+    t0 = time.perf_counter()
+    run = run_gk(op, cfg)
+    ctx.sync()
+    t1 = time.perf_counter()
+    try:
+        out = {"gk_loop": 1e3 * (t1 - t0), "gk_steps": run.k_prime}
+        if W["kind"] != "fsvd":
+            _lib.bidiag_sv2(run.alphas, run.betas)
+            out["spectral"] = 1e3 * (time.perf_counter() - t1)
+            return out
+        theta, G = symtridiag_eig(_gram(run.alphas, run.betas))
+        t2 = time.perf_counter()
+        take = min(W["r"], run.k_prime)
+        sig = np.ascontiguousarray(np.sqrt(np.maximum(theta[:take], 0.0)))
+        Gt = np.ascontiguousarray(G[:, :take].T)
+        Ub = np.empty((take, op.m_local))
+        Vb = np.empty((take, W["n"]))
+        good = C.c_int()
+        _lib.check(_lib.load_library().ksvd_ritz(run.handle, _lib.dptr(Gt), _lib.dptr(sig),
+                                                take, 1, _lib.dptr(Ub), _lib.dptr(Vb),
+                                                C.byref(good)))
+        ctx.sync()
+        t3 = time.perf_counter()
+        out.update({"spectral": 1e3 * (t2 - t1), "ritz_u_recovery_and_download": 1e3 * (t3 - t2)})
+        return out
+    finally:
+        run.free()
+
+
 class ClockSampler:
     """SM clocks and throttle reasons sampled during the timed region."""
 
@@ -389,6 +433,11 @@ def run_ours(args, rank, world, dist):
         e2e = {"value": sum(kps_e2e) / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms / args.steps, "kind": kind}
 
+    # ---- stages of one call (GK loop, spectral stage, Ritz/U
+    # recovery reported separately): host wall time with a sync after each
+    stages = stage_breakdown(K, W, op, ctx)
+    barrier()
+
     # ---- config 1 as BASELINE words it: top-10 to convergence tol 1e-10 with
     # Krylov dimension 30 -- the restarted mode (the
     # reference has no restarts, so its call above stops unconverged)
@@ -444,6 +493,7 @@ def run_ours(args, rank, world, dist):
             "e2e": e2e,
             "gpu_launches": launches,
             "converged_top_k": converged,
+            "stages_ms": stages,
             "clocks": clk.summary(),
         }
         emit(line)

@@ -60,6 +60,8 @@ def test_bench_stdout_is_one_json_line_with_nccl():
     line = json.loads(lines[0])
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
                 "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
-                "roofline", "e2e", "gpu_launches", "clocks"):
+                "roofline", "e2e", "gpu_launches", "clocks", "stages_ms"):
         assert key in line, key
     assert line["value"] > 0 and line["gpu_launches"] > 0
+    st = line["stages_ms"]
+    assert st["gk_loop"] > 0 and st["spectral"] >= 0 and st["ritz_u_recovery_and_download"] > 0
