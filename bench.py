@@ -488,6 +488,8 @@ def run_ours(args, rank, world, dist):
             "time_to_result_s": ms / args.steps / 1e3,
             "gk_steps_per_call": kps[0] if kps else None,
             "effective_GBps": eff_gbps,
+            # 2 m n bytes per GK step over the whole call vs the aggregate HBM peak
+            "effective_frac_of_hbm_peak": eff_gbps / (peak * world),
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
