@@ -27,6 +27,10 @@ def lib():
                                         C.c_int64, C.c_int64, C.c_int, pd]
         _lib.ksvd_host_normal.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64]
         _lib.ksvd_host_normal.restype = C.c_double
+        _lib.ksvd_host_gemv_f32.argtypes = [C.c_void_p, C.c_int64, C.c_int64, pd, pd]
+        _lib.ksvd_host_gemv_t_f32.argtypes = [C.c_void_p, C.c_int64, C.c_int64, pd, pd]
+        _lib.ksvd_host_gauss.argtypes = [C.c_uint64, C.c_uint32, C.c_int64, C.c_int64, C.c_int,
+                                         pd]
     return _lib
 
 
@@ -52,3 +56,48 @@ class GeneratedRows:
                              self.noise, self.seed, i0, i1, int(self.f32),
                              out.ctypes.data_as(pd))
         return out
+
+
+TAG_LEFT, TAG_RIGHT = 2, 3  # include/ksvd_gen.h stream tags
+
+
+def host_gauss(seed: int, tag: int, row0: int, rows: int, r: int) -> np.ndarray:
+    """rows x r Gaussians of the generator's factor stream, bit-identical to
+    the device's k_gen_gauss (include/ksvd_gen.h)."""
+    out = np.empty((rows, r))
+    lib().ksvd_host_gauss(int(seed), int(tag), int(row0), int(rows), int(r),
+                          out.ctypes.data_as(C.POINTER(C.c_double)))
+    return out
+
+
+def _cholqr2(X: np.ndarray) -> np.ndarray:
+    for _ in range(2):
+        L = np.linalg.cholesky(X.T @ X)
+        X = np.linalg.solve(L, X.T).T
+    return X
+
+
+def spectrum(spec) -> np.ndarray:
+    """s_1..s_r of a GenSpec (csrc/ksvd.cu generate_into)."""
+    i = np.arange(1, spec.rank + 1, dtype=np.float64)
+    if spec.spectrum == "harmonic":
+        return spec.s0 / i
+    if spec.spectrum == "exp":
+        return spec.s0 * np.exp(-i / spec.p)
+    if spec.rank == 1:
+        return np.array([spec.s0])
+    return spec.s0 * 10.0 ** (-spec.p * (i - 1) / (spec.rank - 1))
+
+
+def host_generated_rows(spec, row0: int, rows: int) -> "GeneratedRows":
+    """Rows [row0, row0 + rows) of a generated configuration rebuilt on the
+    host alone (no GPU): the factor Gaussians are the device's bit for bit,
+    the CholeskyQR2 runs in numpy, so entries agree with the device matrix
+    to rounding of the orthonormal factors (~1e-15 relative), not bitwise.
+    Used for the reference arm's CPU timing sample, where the values only
+    have to be the configuration's."""
+    r = spec.rank
+    P = _cholqr2(host_gauss(spec.seed, TAG_LEFT, 0, spec.m, r))
+    Q = _cholqr2(host_gauss(spec.seed, TAG_RIGHT, 0, spec.n, r))
+    ps = P[row0:row0 + rows] * spectrum(spec)
+    return GeneratedRows(ps, Q, spec.noise, spec.seed, spec.dtype == "f32", row0=row0)

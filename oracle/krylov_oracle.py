@@ -300,23 +300,32 @@ class OraclePsvd:
 
 
 def fsvd_oracle(A, k, r, eps=1e-8, seed=0, reorth_passes=2, orthonormalize_u=True,
-                start_mean=2.0, start_std=1.0) -> OraclePsvd:
-    """Partial SVD (fsvd.py:158-204)."""
+                start_mean=2.0, start_std=1.0, timings: dict | None = None) -> OraclePsvd:
+    """Partial SVD (fsvd.py:158-204).  `timings` (optional) receives the
+    wall seconds of the stages: gk, spectral, ritz_v (V = P G, n-sized) and
+    ritz_u (the U products, filter and signs, m-sized)."""
+    import time
+
+    tick = time.perf_counter
     op = as_op(A)
     m, n = op.shape
     if not 1 <= r <= k <= min(m, n):
         raise OracleConfigError(f"need 1 <= r <= k <= min(m,n); got r={r}, k={k}")
+    t0 = tick()
     g = gk_oracle(op, k, eps=eps, reorth_passes=reorth_passes, start_mean=start_mean,
                   start_std=start_std, seed=seed)
+    t1 = tick()
     if g.degenerate:
         return OraclePsvd(np.zeros((m, 0)), np.zeros(0), np.zeros((n, 0)), True, 0, g,
                           np.zeros(0))
     theta, G = ql_eig(*gram_of(g.alphas, g.betas))
+    t2 = tick()
     top = math.sqrt(max(float(theta[0]), 0.0))
     keep = int(np.count_nonzero(theta > (DROP_REL * top) ** 2))
     take = min(r, keep)
     sig = np.sqrt(theta[:take])
     V = g.P @ G[:, :take]
+    t3 = tick()
     U = np.empty((m, take))
     for j in range(take):  # the reference's `take` separate products
         U[:, j] = op.apply(V[:, j]) / sig[j]
@@ -325,6 +334,8 @@ def fsvd_oracle(A, k, r, eps=1e-8, seed=0, reorth_passes=2, orthonormalize_u=Tru
         if good < take:
             take, sig, V = good, sig[:good], V[:, :good]
     U, V = signs_fixed(U, V)
+    if timings is not None:
+        timings.update(gk=t1 - t0, spectral=t2 - t1, ritz_v=t3 - t2, ritz_u=tick() - t3)
     return OraclePsvd(U, sig, V, take < r, min(r, g.k_prime) - take, g, theta)
 
 
@@ -335,6 +346,7 @@ class OracleRank:
     eigenvalues: np.ndarray
     threshold: float
     mode: str
+    gk: GKResult | None = None
 
 
 def threshold_count(theta, eps, mode):
@@ -353,18 +365,28 @@ def threshold_count(theta, eps, mode):
 
 
 def rank_oracle(A, eps=1e-8, mode="absolute", seed=0, reorth_passes=2, gk_eps=1e-8,
-                start_mean=2.0, start_std=1.0) -> OracleRank:
+                start_mean=2.0, start_std=1.0, k_max: int | None = None,
+                timings: dict | None = None) -> OracleRank:
     """Numerical rank (rank.py:51-67): GK to min(m, n), eigenvalues without
-    vectors, strict count."""
+    vectors, strict count.  `k_max` caps the loop below min(m, n) (timing
+    samples only -- the reference always runs to min(m, n)); `timings`
+    receives the stage seconds (gk, spectral)."""
+    import time
+
     if mode not in ("absolute", "relative"):
         raise OracleConfigError(f"mode {mode!r}")
     if not eps > 0:
         raise OracleConfigError("eps must be > 0")
     op = as_op(A)
-    g = gk_oracle(op, min(op.shape), eps=gk_eps, reorth_passes=reorth_passes,
-                  start_mean=start_mean, start_std=start_std, seed=seed)
+    t0 = time.perf_counter()
+    g = gk_oracle(op, min(op.shape) if k_max is None else k_max, eps=gk_eps,
+                  reorth_passes=reorth_passes, start_mean=start_mean, start_std=start_std,
+                  seed=seed)
+    t1 = time.perf_counter()
     if g.degenerate:
-        return OracleRank(0, 0, np.zeros(0), eps if mode == "absolute" else 0.0, mode)
+        return OracleRank(0, 0, np.zeros(0), eps if mode == "absolute" else 0.0, mode, g)
     theta, _ = ql_eig(*gram_of(g.alphas, g.betas), vectors=False)
     cnt, thr = threshold_count(theta, eps, mode)
-    return OracleRank(cnt, g.k_prime, theta, thr, mode)
+    if timings is not None:
+        timings.update(gk=t1 - t0, spectral=time.perf_counter() - t1)
+    return OracleRank(cnt, g.k_prime, theta, thr, mode, g)

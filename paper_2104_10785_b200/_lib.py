@@ -220,6 +220,16 @@ def get_context() -> Context:
     return _ctx
 
 
+def device_count() -> int:
+    """CUDA devices visible to this process (0 when none or no driver)."""
+    n = C.c_int()
+    try:
+        check(load_library().ksvd_device_count(C.byref(n)))
+    except RuntimeError:
+        return 0
+    return int(n.value)
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(NCCL_UID_BYTES)
     check(load_library().ksvd_nccl_unique_id(buf))

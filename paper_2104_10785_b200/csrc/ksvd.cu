@@ -110,6 +110,10 @@ struct ksvd_ctx {
   HostProg* dprog = nullptr;  // device view of the same memory
   cudaEvent_t ring_ev[8] = {};
   unsigned long long* tdbg = nullptr;  // KSVD_PHASE_TIMES: CGS phase timing
+  // pinned staging ring for pageable host <-> device matrix transfers
+  void* stage[2] = {nullptr, nullptr};
+  size_t stage_bytes = 0;
+  cudaEvent_t stage_ev[2] = {};
 };
 
 static int get_event(ksvd_ctx* c, cudaEvent_t* ev) {
@@ -2174,6 +2178,10 @@ int ksvd_ctx_destroy(ksvd_ctx* c) {
   for (auto e : c->marks) cudaEventDestroy(e);
   for (auto e : c->ring_ev) cudaEventDestroy(e);
   if (c->hprog) cudaFreeHost(c->hprog);
+  for (int b = 0; b < 2; ++b) {
+    if (c->stage[b]) cudaFreeHost(c->stage[b]);
+    if (c->stage_ev[b]) cudaEventDestroy(c->stage_ev[b]);
+  }
   cudaStreamDestroy(c->stream);
   delete c;
   return 0;
@@ -2339,6 +2347,110 @@ int ksvd_ctx_elapsed(ksvd_ctx* c, int s0, int s1, float* ms) {
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// Host <-> device matrix transfers.  A pinned source/destination is one DMA;
+// a pageable one (a plain numpy array) would go through the driver's own
+// small bounce buffer at a fraction of the link rate, so it is staged here
+// through a ring of two pinned chunks: io threads copy rows between the user
+// buffer and chunk b while the DMA engine moves chunk b^1.
+static bool host_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+static int ensure_stage(ksvd_ctx* c, size_t bytes) {
+  if (c->stage_bytes >= bytes) return 0;
+  CK(cudaStreamSynchronize(c->stream));
+  for (int b = 0; b < 2; ++b) {
+    if (c->stage[b]) CK(cudaFreeHost(c->stage[b]));
+    c->stage[b] = nullptr;
+    CK(cudaHostAlloc(&c->stage[b], bytes, cudaHostAllocDefault));
+    if (!c->stage_ev[b]) CK(cudaEventCreateWithFlags(&c->stage_ev[b], cudaEventDisableTiming));
+  }
+  c->stage_bytes = bytes;
+  return 0;
+}
+
+// bytes [lo, lo + len) of `rows` packed rows of `width` bytes, between the
+// packed chunk `pk` and the strided user rows `u` (pitch `up`)
+static void copy_packed(char* pk, char* u, size_t up, size_t width, size_t lo, size_t len,
+                        bool to_packed) {
+  while (len) {
+    const size_t r = lo / width, off = lo % width, n = std::min(len, width - off);
+    char* a = pk + lo;
+    char* b = u + r * up + off;
+    if (to_packed) memcpy(a, b, n);
+    else memcpy(b, a, n);
+    lo += n;
+    len -= n;
+  }
+}
+
+static int staged_copy(ksvd_ctx* c, void* dev, size_t dpitch, void* host, size_t hpitch,
+                       size_t width, int64_t rows, bool to_device) {
+  if (rows <= 0) return 0;
+  cudaStream_t s = c->stream;
+  if (host_pinned(host)) {
+    CK(cudaMemcpy2DAsync(to_device ? dev : host, to_device ? dpitch : hpitch,
+                         to_device ? host : dev, to_device ? hpitch : dpitch, width,
+                         (size_t)rows, to_device ? cudaMemcpyHostToDevice
+                                                 : cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return 0;
+  }
+  const size_t chunk = std::max<size_t>((size_t)io_chunk_bytes(), width);
+  const int64_t rpc = (int64_t)(chunk / width);
+  TRY(ensure_stage(c, (size_t)rpc * width));
+  char* d = static_cast<char*>(dev);
+  char* h = static_cast<char*>(host);
+  int64_t pend_r = -1, pend_n = 0;  // D2H: chunk waiting to be copied out
+  int pend_b = 0;
+  auto drain = [&]() -> bool {
+    if (pend_r < 0) return true;
+    if (cudaEventSynchronize(c->stage_ev[pend_b]) != cudaSuccess) return false;
+    char* pk = static_cast<char*>(c->stage[pend_b]);
+    char* u = h + (size_t)pend_r * hpitch;
+    io_parallel((size_t)pend_n * width, [&](size_t lo, size_t len) {
+      copy_packed(pk, u, hpitch, width, lo, len, false);
+      return true;
+    });
+    pend_r = -1;
+    return true;
+  };
+  int k = 0;
+  for (int64_t r = 0; r < rows; r += rpc, ++k) {
+    const int b = k & 1;
+    const int64_t nr = std::min(rpc, rows - r);
+    char* pk = static_cast<char*>(c->stage[b]);
+    if (to_device) {
+      if (k >= 2) CK(cudaEventSynchronize(c->stage_ev[b]));  // chunk b's DMA is done
+      char* u = h + (size_t)r * hpitch;
+      io_parallel((size_t)nr * width, [&](size_t lo, size_t len) {
+        copy_packed(pk, u, hpitch, width, lo, len, true);
+        return true;
+      });
+      CK(cudaMemcpy2DAsync(d + (size_t)r * dpitch, dpitch, pk, width, width, (size_t)nr,
+                           cudaMemcpyHostToDevice, s));
+      CK(cudaEventRecord(c->stage_ev[b], s));
+    } else {
+      CK(cudaMemcpy2DAsync(pk, width, d + (size_t)r * dpitch, dpitch, width, (size_t)nr,
+                           cudaMemcpyDeviceToHost, s));
+      CK(cudaEventRecord(c->stage_ev[b], s));
+      if (!drain()) return set_err(KSVD_ERUNTIME, "staged download failed");
+      pend_r = r;
+      pend_n = nr;
+      pend_b = b;
+    }
+  }
+  if (!drain()) return set_err(KSVD_ERUNTIME, "staged download failed");
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
 static int matrix_new(ksvd_ctx* c, const void* rows, int64_t m, int64_t n, int64_t row0,
                       int64_t mloc, int64_t src_ld, int dtype, cudaMemcpyKind kind,
                       ksvd_mat** out) {
@@ -2383,15 +2495,24 @@ static int matrix_new(ksvd_ctx* c, const void* rows, int64_t m, int64_t n, int64
         return set_err(KSVD_ERUNTIME, "memset: %s", cudaGetErrorString(e));
       }
     }
-    cudaError_t e =
-        (src_ld == n && M->lda == n)  // contiguous on both sides: one linear DMA
-            ? cudaMemcpyAsync(M->A, rows, (size_t)mloc * n * es, kind, c->stream)
-            : cudaMemcpy2DAsync(M->A, (size_t)M->lda * es, rows, (size_t)src_ld * es,
-                                (size_t)n * es, (size_t)mloc, kind, c->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-    if (e != cudaSuccess) {
-      free_matrix(M);
-      return set_err(KSVD_ERUNTIME, "matrix upload: %s", cudaGetErrorString(e));
+    if (kind == cudaMemcpyHostToDevice) {
+      rc = staged_copy(c, M->A, (size_t)M->lda * es, const_cast<void*>(rows),
+                       (size_t)src_ld * es, (size_t)n * es, mloc, true);
+      if (rc) {
+        free_matrix(M);
+        return rc;
+      }
+    } else {
+      cudaError_t e =
+          (src_ld == n && M->lda == n)  // contiguous on both sides: one linear copy
+              ? cudaMemcpyAsync(M->A, rows, (size_t)mloc * n * es, kind, c->stream)
+              : cudaMemcpy2DAsync(M->A, (size_t)M->lda * es, rows, (size_t)src_ld * es,
+                                  (size_t)n * es, (size_t)mloc, kind, c->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+      if (e != cudaSuccess) {
+        free_matrix(M);
+        return set_err(KSVD_ERUNTIME, "matrix upload: %s", cudaGetErrorString(e));
+      }
     }
   }
   *out = M;
@@ -2631,10 +2752,8 @@ int ksvd_matrix_to_host(ksvd_mat* M, void* rows) {
   CK(cudaSetDevice(c->device));
   if (M->mloc == 0) return 0;
   const size_t es = esize(M->dtype);
-  CK(cudaMemcpy2DAsync(rows, (size_t)M->n * es, M->A, (size_t)M->lda * es, (size_t)M->n * es,
-                       (size_t)M->mloc, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  return 0;
+  return staged_copy(c, M->A, (size_t)M->lda * es, rows, (size_t)M->n * es, (size_t)M->n * es,
+                     M->mloc, false);
 }
 
 static int reset_state(ksvd_ctx* c, DevState* st) {

@@ -104,6 +104,14 @@ def dense_svd(A) -> PartialSvd:
     return PartialSvd(U=U, sigma=s, V=V)
 
 
+def triplet_quality(oracle: PartialSvd, method_psvd: PartialSvd, name: str) -> TripletQuality:
+    """q_j = <u_j, u_j'> <v_j, v_j'> against the oracle (bench.py:79-85)."""
+    r = min(oracle.rank, method_psvd.rank)
+    qu = np.einsum("ij,ij->j", oracle.U[:, :r], method_psvd.U[:, :r])
+    qv = np.einsum("ij,ij->j", oracle.V[:, :r], method_psvd.V[:, :r])
+    return TripletQuality(name, qu * qv, oracle.sigma[:r].copy(), method_psvd.sigma[:r].copy())
+
+
 def run_method(method: str, A, r: int, rank_true: int | None, seed: int,
                k: int | None = None, power_iters: int = 0,
                oversampling: int | None = None) -> dict:

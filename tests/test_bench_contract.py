@@ -65,3 +65,46 @@ def test_bench_stdout_is_one_json_line_with_nccl():
     assert line["value"] > 0 and line["gpu_launches"] > 0
     st = line["stages_ms"]
     assert st["gk_loop"] > 0 and st["spectral"] >= 0 and st["ritz_u_recovery_and_download"] > 0
+
+
+def test_rank_envs():
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    envs = bench.rank_envs(2, 12345, base={"PATH": "/bin"})
+    assert [e["RANK"] for e in envs] == ["0", "1"]
+    assert [e["LOCAL_RANK"] for e in envs] == ["0", "1"]
+    assert all(e["WORLD_SIZE"] == "2" and e["MASTER_ADDR"] == "127.0.0.1"
+               and e["MASTER_PORT"] == "12345" and e["NCCL_DEBUG"] == "INFO" for e in envs)
+    one = bench.rank_envs(1, 1, base={})[0]
+    assert one["WORLD_SIZE"] == "1" and "NCCL_DEBUG" not in one
+
+
+@pytest.mark.timeout(300)
+def test_launcher_env_plumbing(tmp_path):
+    """bench.launch() at N=2 (what `bench.py --gpus 2` does) on CPU: both
+    ranks rendezvous over gloo from the environment it sets."""
+    code = ("import sys, bench; sys.exit(bench.launch(2, [sys.argv[1]], "
+            "script='tests/launch_probe.py', check_gpus=False))")
+    res = subprocess.run([sys.executable, "-c", code, str(tmp_path)], cwd=ROOT,
+                         capture_output=True, text=True, timeout=280)
+    assert res.returncode == 0, res.stderr[-2000:]
+    recs = [json.loads((tmp_path / f"rank{r}.json").read_text()) for r in range(2)]
+    assert [r["RANK"] for r in recs] == ["0", "1"]
+    assert all(r["sum"] == 3.0 and r["WORLD_SIZE"] == "2" for r in recs)
+    assert res.stdout.strip() == "rank0-stdout"
+
+
+def test_launcher_refuses_missing_gpus():
+    """More GPUs asked for than visible: non-zero exit, no JSON line."""
+    res = subprocess.run([sys.executable, "bench.py", "--gpus", "64", "--config", "1"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=120)
+    assert res.returncode != 0 and res.stdout.strip() == ""
+    assert "GPU(s) visible" in res.stderr
+
+
+def test_world_size_mismatch_refused():
+    env = {**__import__("os").environ, "WORLD_SIZE": "2", "RANK": "0"}
+    res = subprocess.run([sys.executable, "bench.py", "--gpus", "1", "--config", "1"],
+                         cwd=ROOT, env=env, capture_output=True, text=True, timeout=120)
+    assert res.returncode == 2 and "WORLD_SIZE" in res.stderr
