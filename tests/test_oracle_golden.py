@@ -7,6 +7,7 @@ CPU only.
 """
 
 import math
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -133,3 +134,24 @@ def test_readme_known_answer():
 
     rep = O.rank_oracle(low_rank_synth(1000, 1000, 100, seed=0), seed=0)
     assert (rep.rank, rep.k_prime) == (100, 102)
+
+
+def test_fullsize_config5_fixture_pins_the_rank_deviation():
+    """tests/golden/full_c5.npz (the oracle on the downloaded full config-5
+    matrix): the reference's QL count on the oracle's alphas/betas is 301,
+    the oracle's QL restatement agrees, while a relatively accurate SVD of
+    the SAME alphas/betas (libksvd host code) counts the planted 300 -- the
+    301st value sits at QL's error bound, not in the matrix."""
+    from paper_2104_10785_b200 import _lib
+    from paper_2104_10785_b200.rank import count_above
+
+    g = dict(np.load(Path(__file__).resolve().parent / "golden" / "full_c5.npz"))
+    a, b = g["oracle_alphas"], g["oracle_betas"]
+    theta_ql, _ = O.ql_eig(*O.gram_of(a, b), vectors=False)
+    assert O.threshold_count(theta_ql, 1e-8, "relative")[0] == 301
+    assert int(g["reference_ql_rank_on_oracle"]) == 301
+    np.testing.assert_allclose(theta_ql, g["reference_ql_theta_on_oracle"], rtol=0,
+                               atol=1e-15 * theta_ql[0])
+    acc = _lib.bidiag_sv2(a, b)
+    assert count_above(acc, 1e-8, "relative")[0] == 300
+    assert acc[300] / acc[0] < 1e-17 < theta_ql[300] / theta_ql[0] - 1e-16
