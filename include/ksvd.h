@@ -116,7 +116,8 @@ int ksvd_px_enabled(ksvd_ctx *ctx, int *on);
 /* ---- matrices ----------------------------------------------------------
  * rows: host pointer to the m_local local rows (row-major, src_ld elements
  * between rows) of the global m x n matrix; row0 = first global row.
- * Device layout: row-major, leading dimension padded to 512 B, padding 0. */
+ * Device layout: row-major, leading dimension padded to a 16-byte multiple
+ * (KSVD_LDA_BYTES overrides), padding 0. */
 int ksvd_matrix_from_host(ksvd_ctx *ctx, const void *rows, int64_t m_global,
                           int64_t n, int64_t row0, int64_t m_local,
                           int64_t src_ld, int dtype, ksvd_mat **out);
@@ -146,7 +147,11 @@ int ksvd_matmat(ksvd_mat *mat, const double *X, int k, double *Y);
 int ksvd_gk_run(ksvd_mat *mat, int k_max, double eps, int reorth_passes,
                 const double *q1_local, ksvd_run **out);
 /* alphas: capacity k_max, betas: capacity k_max+1 (betas[0] is filled
- * by the caller; the library writes betas[1..k']) */
+ * by the caller; the library writes alphas[0..k'-1] and betas[1..k'], i.e.
+ * beta_{k'+1} included -- the sub-threshold value on a beta breakdown).  On
+ * an alpha breakdown (k' < k_max) alphas[k'] receives the sub-threshold
+ * alpha_{k'+1}, which the reference drops (bidiag.py:174-176); callers
+ * that mirror the reference read alphas[0..k'-1] only. */
 int ksvd_run_info(ksvd_run *run, int *k_prime, int *flags, double *alphas,
                   double *betas);
 /* Terminal column (bidiag.py:95-108), one attempt: v = (v_local or the

@@ -44,9 +44,9 @@ def restarted_oracle(A, r, k, tol=1e-10, max_restarts=100, keep=None, eps=1e-8,
         if head is not None:
             T[:l, :l] = np.diag(head[0])
             T[:l, l] = head[1]
-        kp, beta_next, alpha_break = k, 0.0, False
+        kp, beta_next, alpha_break, alpha_next = k, 0.0, False, 0.0
         if a < eps:
-            kp, alpha_break = l, True
+            kp, alpha_break, alpha_next = l, True, a
         else:
             T[l, l] = a
             P[:, l] = z / a
@@ -56,7 +56,7 @@ def restarted_oracle(A, r, k, tol=1e-10, max_restarts=100, keep=None, eps=1e-8,
                 b = float(np.linalg.norm(w))
                 steps += 1
                 if b < eps:
-                    kp = i
+                    kp, beta_next = i, b
                     break
                 Q[:, i] = w / b
                 if i == k:
@@ -66,7 +66,7 @@ def restarted_oracle(A, r, k, tol=1e-10, max_restarts=100, keep=None, eps=1e-8,
                 z = _reorth(z, P[:, :i], reorth_passes)
                 a = float(np.linalg.norm(z))
                 if a < eps:
-                    kp, alpha_break = i, True
+                    kp, alpha_break, alpha_next = i, True, a
                     T[i - 1, i] = b
                     break
                 T[i - 1, i] = b
@@ -77,7 +77,10 @@ def restarted_oracle(A, r, k, tol=1e-10, max_restarts=100, keep=None, eps=1e-8,
         Uh, s, Vht = np.linalg.svd(Ts)
         Vh = Vht.T
         early = kp < k or alpha_break
-        resid = np.zeros(size) if early else abs(beta_next) * np.abs(Uh[kp - 1, :])
+        # residual of each Ritz triplet: beta_{k'+1} |Uh[k'-1, i]| (A v - s u),
+        # or after an alpha breakdown alpha_{k'+1} |Vh[k', i]| (A^T u - s v)
+        resid = (abs(alpha_next) * np.abs(Vh[kp, :]) if alpha_break
+                 else abs(beta_next) * np.abs(Uh[kp - 1, :]))
         s1 = float(s[0]) if s.size else 0.0
         take = min(r, int((s > 1e-14 * s1).sum()))
         if early or np.all(resid[:take] <= tol * s1) or restarts >= max_restarts:

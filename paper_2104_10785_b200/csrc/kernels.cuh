@@ -49,26 +49,14 @@ struct HostProg {
   int pad;
 };
 
-// 1 when the host paces on the progress word (KSVD_PACE=spin); otherwise it
-// waits on events and reads only halt_step after them, so a breakdown needs
-// plain stores (visible once the kernel has completed) and the per-step
-// prog word -- a system-scope release store at the tail of every alpha-side
-// CGS kernel, on the step's critical path -- is not written at all.
-__constant__ int g_spin_pace = 0;
-
-// publish a norm test's outcome to the host (breakdowns always; in spin
-// mode also the step's last test, side 1, with a release store ordering
-// the status words before prog)
+// publish a breakdown to the host (plain stores to mapped memory, visible
+// once the kernel has completed; the host reads them after its pacing event)
 __device__ __forceinline__ void host_progress(HostProg* hp, int stop, int step, int side) {
-  if (!hp) return;
-  if (stop != 0) {
-    volatile HostProg* h = hp;
-    h->status = stop;
-    h->halt_step = step;
-  }
-  if (g_spin_pace && (stop != 0 || side == 1))
-    asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(&hp->prog), "r"(2 * step + side)
-                 : "memory");
+  (void)side;
+  if (!hp || stop == 0) return;
+  volatile HostProg* h = hp;
+  h->status = stop;
+  h->halt_step = step;
 }
 
 // Programmatic dependent launch (ksvd.cu launch_step): wait for the
@@ -76,15 +64,12 @@ __device__ __forceinline__ void host_progress(HostProg* hp, int stop, int step, 
 // Every CTA of a kernel launched with the attribute calls pdl_wait() before
 // reading its predecessor's outputs and before exiting.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-// g_pdl_trig bit 0: gemv kernels trigger early, bit 1: CGS kernels do
-// (otherwise the trigger is implicit at CTA exit); KSVD_PDL_TRIG overrides.
-// Measured: 1 is best -- an early CGS trigger parks the next gemv's CTAs
-// beside the cooperative grid and costs ~5% on config 2.
-// (constant bank: a global load here sat in front of every kernel's first
-// loads, the asm's memory clobber keeping them behind it)
-__constant__ int g_pdl_trig = 1;
+// bit 1: the gemv kernels trigger their dependents early (right after their
+// own wait); bit 2 (CGS kernels) stays implicit at CTA exit -- measured, an
+// early CGS trigger parks the next gemv's CTAs beside the grid-synchronised
+// CGS kernel and costs ~5% on config 2.
 __device__ __forceinline__ void pdl_trigger(int bit) {
-  if (g_pdl_trig & bit) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (bit & 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 __device__ __forceinline__ bool halted(const DevState* st) {
@@ -215,10 +200,9 @@ __device__ __forceinline__ double ldv(const double* p) {
   else return *p;
 }
 
-// The body is a device function so the persistent streaming kernel
-// (stream.cuh) runs the same code with the same work decomposition; p, its
-// scale and the partials go through L2 (__ldcg): inside a persistent kernel
-// they were written by other CTAs of the same launch.
+// The body is a device function; CG = true sends p, its scale and the
+// partials through L2 (__ldcg), for callers whose other CTAs wrote them in
+// the same launch.
 template <typename TA, int U, int RB = 8, int PF = 0, bool CG = false>
 __device__ __forceinline__ void gemv_n2_body(const TA* __restrict__ A, int64_t lda, int64_t m,
                                              int64_t nvec, int nchunks, int64_t nseg,
@@ -309,161 +293,6 @@ k_gemv_n2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nc
   if (halted(st)) return;
   gemv_n2_body<TA, U, RB, PF>(A, lda, m, nvec, nchunks, nseg, p_src, p_scale, p_dst, n_true,
                               part, (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5));
-}
-
-// ---------------------------------------------------------------------------
-// gemv_n, TMA-fed (k_gemv_n3): w = A p   (bidiag.py:152)
-//
-// Persistent: one CTA per SM, 8 consumer warps + 1 producer warp.  Work
-// units are (column group of 8 chunks, 8 consecutive rows); CTA b takes the
-// contiguous unit range [b*N/G, (b+1)*N/G), so units walk down the rows of
-// one column group.  The producer streams each unit -- 8 row segments of
-// 8 KB, one bulk-async copy (cp.async.bulk) per row -- into a 3-stage
-// shared-memory ring guarded by full/empty mbarriers; consumer warp w owns
-// chunk w of the group: its slice of p sits in registers, it reads its
-// 1 KB of each row from shared memory, forms the 8 row partials and reduces
-// them with one warp_sum8.  A never passes through registers in flight, so
-// the kernel keeps 128 KB of loads outstanding per SM at low register cost.
-// Output layout = k_gemv_n2 (part[chunk*m + row]).
-constexpr int kN3Stages = 3;
-constexpr int kN3Rows = 8;
-constexpr int kN3Group = 8;       // chunks per column group = consumer warps
-constexpr int kN3U = 2;           // 16-byte vectors per lane per row
-constexpr int kN3CW = 32 * kN3U;  // vectors per chunk (1 KB)
-constexpr int kN3Threads = (kN3Group + 1) * 32;
-constexpr size_t kN3StageBytes = (size_t)kN3Rows * kN3Group * kN3CW * 16;  // 64 KB
-constexpr size_t kN3Smem = kN3Stages * kN3StageBytes;
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
-                                         uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(dst),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-
-template <typename TA>
-__global__ void __launch_bounds__(kN3Threads, 1)
-k_gemv_n3(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nchunks,
-          int64_t rows8, int64_t units, const double* __restrict__ p_src,
-          const double* __restrict__ p_scale, double* __restrict__ p_dst, int64_t n_true,
-          double* __restrict__ part, const DevState* st) {
-  if (halted(st)) return;
-  constexpr int V = AVec<TA>::V;
-  extern __shared__ __align__(1024) unsigned char n3_smem[];
-  __shared__ __align__(8) unsigned long long full[kN3Stages], empty[kN3Stages];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t G = gridDim.x;
-  const int64_t u0 = units * blockIdx.x / G, u1 = units * (blockIdx.x + 1) / G;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kN3Stages; ++s) {
-      mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), kN3Group);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  if (warp == kN3Group) {  // ---- producer
-    if (lane == 0) {
-      for (int64_t u = u0, it = 0; u < u1; ++u, ++it) {
-        const int s = (int)(it % kN3Stages);
-        const int64_t round = it / kN3Stages;
-        if (round > 0)
-          while (!mbar_try_wait(smem_u32(&empty[s]), (uint32_t)((round - 1) & 1))) {
-          }
-        const int64_t g = u / rows8, r0 = (u % rows8) * kN3Rows;
-        const int nr = (int)(m - r0 < kN3Rows ? m - r0 : kN3Rows);
-        const int64_t v0 = g * kN3Group * kN3CW;
-        const int64_t wv = nvec - v0 < kN3Group * kN3CW ? nvec - v0 : (int64_t)kN3Group * kN3CW;
-        const uint32_t bytes = (uint32_t)(wv * 16);
-        const uint32_t fb = smem_u32(&full[s]);
-        mbar_expect_tx(fb, bytes * (uint32_t)nr);
-        unsigned char* stage = n3_smem + (size_t)s * kN3StageBytes;
-        for (int rr = 0; rr < nr; ++rr)
-          bulk_g2s(smem_u32(stage + (size_t)rr * kN3Group * kN3CW * 16),
-                   A + (r0 + rr) * lda + v0 * V, bytes, fb);
-      }
-    }
-    return;
-  }
-
-  // ---- consumers: warp = chunk within the group
-  int64_t cur_g = -1;
-  double pv[kN3U][V];
-  bool live[kN3U];
-  for (int64_t u = u0, it = 0; u < u1; ++u, ++it) {
-    const int s = (int)(it % kN3Stages);
-    const int64_t round = it / kN3Stages;
-    const int64_t g = u / rows8, r0 = (u % rows8) * kN3Rows;
-    const int64_t chunk = g * kN3Group + warp;
-    if (g != cur_g) {  // this warp's slice of p (p = p_src / *p_scale)
-      cur_g = g;
-      const double scale = p_scale ? *p_scale : 1.0;
-#pragma unroll
-      for (int uu = 0; uu < kN3U; ++uu) {
-        const int64_t vi = chunk * kN3CW + uu * 32 + lane;
-        live[uu] = chunk < nchunks && vi < nvec;
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-          const int64_t col = vi * V + k;
-          double x = (live[uu] && col < n_true) ? p_src[col] : 0.0;
-          if (p_scale) {
-            x = x / scale;
-            if (r0 == 0 && p_dst && live[uu] && col < n_true) p_dst[col] = x;
-          }
-          pv[uu][k] = x;
-        }
-      }
-    }
-    while (!mbar_try_wait(smem_u32(&full[s]), (uint32_t)(round & 1))) {
-    }
-    const TA* stage = reinterpret_cast<const TA*>(n3_smem + (size_t)s * kN3StageBytes);
-    double v[8];
-#pragma unroll
-    for (int rr = 0; rr < kN3Rows; ++rr) {
-      double acc = 0.0;
-      const TA* row = stage + (size_t)rr * kN3Group * kN3CW * V + (size_t)warp * kN3CW * V;
-#pragma unroll
-      for (int uu = 0; uu < kN3U; ++uu) {
-        if (live[uu] && r0 + rr < m) {
-          AVec<TA> a;
-          const TA* p = row + (uu * 32 + lane) * V;
-          if constexpr (V == 2) {
-            const double2 d = *reinterpret_cast<const double2*>(p);
-            a.v[0] = d.x;
-            a.v[1] = d.y;
-          } else {
-            const float4 f = *reinterpret_cast<const float4*>(p);
-            a.v[0] = f.x;
-            a.v[1] = f.y;
-            a.v[2] = f.z;
-            a.v[3] = f.w;
-          }
-#pragma unroll
-          for (int k = 0; k < V; ++k) acc = fma(a.get(k), pv[uu][k], acc);
-        }
-      }
-      v[rr] = acc;
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(smem_u32(&empty[s]));  // stage free for the producer
-    const double t = warp_sum8(v);
-    const int64_t row = r0 + warp_sum8_index(lane);
-    if ((lane & 3) == 0 && row < m && chunk < nchunks) part[chunk * m + row] = t;
-  }
 }
 
 // w[r] = sum_chunks part[c][r] - alpha q[r]  (chunk order fixed)
@@ -957,10 +786,6 @@ struct CgsCoopArgs {
   const double* fp;
   unsigned long long* tdbg;  // nullable: phase timing of CTA 0
   int redundant;  // k_cgs2_tile2: every CTA reduces all partials (else distributed + barrier)
-  // regular launch, flag barrier: CTA b publishes epoch + k in flags[16 b]
-  // (its own 128-byte line) at its k-th barrier; nullptr: bar / cg sync
-  unsigned long long* flags;
-  unsigned long long epoch;
 };
 
 // Grid-wide barrier of the cooperative launch (cooperative_groups: ~1.2 us
@@ -986,9 +811,10 @@ __device__ __forceinline__ void grid_barrier_raw(unsigned* bar, unsigned nblocks
     asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(bar), "r"(nb)
                  : "memory");
     // a regular launch relies on all nblocks CTAs becoming resident (one per
-    // SM, <= #SMs); should they not (an SM-limited MPS client or green
-    // context), fail loudly after ~20 s instead of spinning forever
-    // (KSVD_COOP_LAUNCH=1 selects the driver-checked cooperative launch)
+    // SM, <= #SMs).  ksvd_ctx_create probes that once (residency_probe) and
+    // switches the context to cooperative launches when it does not hold (an
+    // SM-limited MPS client or green context); should it still fail, trap
+    // after ~20 s instead of spinning forever
     unsigned polls = 0;
     unsigned long long t0 = 0;
     do {
@@ -999,8 +825,8 @@ __device__ __forceinline__ void grid_barrier_raw(unsigned* bar, unsigned nblocks
         if (t0 == 0) {
           t0 = now;
         } else if (now - t0 > 20000000000ull) {
-          printf("ksvd: grid barrier of %u CTAs timed out (not all CTAs resident?); "
-                 "KSVD_COOP_LAUNCH=1 selects the cooperative launch\n", nblocks);
+          printf("ksvd: grid barrier of %u CTAs timed out (not all CTAs resident?)\n",
+                 nblocks);
           __trap();
         }
       }
@@ -1009,40 +835,29 @@ __device__ __forceinline__ void grid_barrier_raw(unsigned* bar, unsigned nblocks
   __syncthreads();
 }
 
-// Flag barrier (regular launch, G <= kThreads): no atomics -- CTA b stores
-// its target epoch to its own line, thread t of every CTA polls CTA t's line
-// (ld.acquire.gpu) until it reaches the target, so one release/acquire pair
-// per CTA pair replaces the serialised adds on one word.  Targets increase
-// across barriers and launches (host epoch + per-launch barrier count), so
-// the lines never need resetting.  Same bounded spin as grid_barrier_raw.
-__device__ __forceinline__ void flag_barrier(unsigned long long* flags, unsigned G,
-                                             unsigned long long target) {
-  __syncthreads();
-  if (threadIdx.x == 0)
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(flags + (size_t)blockIdx.x * 16),
-                 "l"(target)
-                 : "memory");
-  if (threadIdx.x < G) {
-    const unsigned long long* f = flags + (size_t)threadIdx.x * 16;
-    unsigned long long v;
-    unsigned polls = 0;
-    unsigned long long t0 = 0;
+// One-off residency probe (ksvd_ctx_create): G CTAs of a kernel using the
+// CGS kernels' shared-memory budget (so one CTA per SM) arrive on a counter
+// and wait for all G with a short bounded spin; any CTA that gives up sets
+// *failed.  Regular launches with software grid barriers are then safe on
+// this context, else it uses cooperative launches.
+__global__ void __launch_bounds__(kThreads, 1)
+k_residency_probe(unsigned* count, int* failed, unsigned G) {
+  extern __shared__ unsigned char probe_smem[];
+  if (threadIdx.x == 0) {
+    probe_smem[0] = 1;
+    atomicAdd(count, 1u);
+    unsigned long long t0, now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    unsigned cur;
     do {
-      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
-      if ((++polls & 0xfffu) == 0) {
-        unsigned long long now;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-        if (t0 == 0) {
-          t0 = now;
-        } else if (now - t0 > 20000000000ull) {
-          printf("ksvd: flag barrier of %u CTAs timed out (not all CTAs resident?); "
-                 "KSVD_COOP_LAUNCH=1 selects the cooperative launch\n", G);
-          __trap();
-        }
+      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(count) : "memory");
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t0 > 200000000ull) {  // 200 ms
+        atomicExch(failed, 1);
+        break;
       }
-    } while (v < target);
+    } while (cur < G);
   }
-  __syncthreads();
 }
 
 // the k-th grid-wide barrier of a CGS launch (k counted per thread: every
@@ -1050,10 +865,7 @@ __device__ __forceinline__ void flag_barrier(unsigned long long* flags, unsigned
 __device__ __forceinline__ void grid_barrier(const CgsCoopArgs& a, unsigned G,
                                              unsigned long long& k) {
   ++k;
-  if (a.flags)
-    flag_barrier(a.flags, G, a.epoch + k);
-  else
-    grid_barrier_raw(a.bar, G);
+  grid_barrier_raw(a.bar, G);
 }
 
 // phase timestamps of CTA 0 (debug builds of the timing breakdown)
@@ -1066,372 +878,20 @@ __device__ __forceinline__ void phase_mark(unsigned long long* t, int k, unsigne
   }
 }
 
-// columns of `part` (ncols x G, column-major in b) summed into c; warps of
-// the whole grid take columns round-robin
-__device__ __forceinline__ void coop_reduce_cols(const double* part, int ncols, int G,
-                                                 double* c) {
-  const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const int nw = gridDim.x * kWarps;
-  for (int j = gw; j < ncols; j += nw) {
-    const double* p = part + (int64_t)j * G;
-    double s = 0.0;
-    for (int b = lane; b < G; b += 32) s += __ldcg(p + b);
-    s = warp_sum(s);
-    if (lane == 0) c[j] = s;
-  }
-}
-
-template <int RPL>
-__global__ void __launch_bounds__(kThreads)
-k_cgs2_coop(CgsCoopArgs a) {
-  pdl_wait();
-  pdl_trigger(2);
-  if (halted(a.st)) return;
-  constexpr int CH = 32 * RPL;  // rows per chunk
-  extern __shared__ double colacc[];  // ncols (dot accumulators)
-  __shared__ double tred[kWarps][CH];
-  __shared__ double nacc;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned G = gridDim.x;
-  unsigned long long bk = 0;  // grid barriers passed in this launch
-  const int64_t s0 = (int64_t)blockIdx.x * a.rows_per_cta;
-  const int64_t s1 = min(a.L, s0 + a.rows_per_cta);
-
-  // [0] finalisation of the split partial sums of A^T q
-  if (a.fpart) {
-    for (int64_t r = s0 + threadIdx.x; r < s1; r += kThreads) {
-      double v = strided_sum(a.fpart + r, a.fld, a.fnsplit);
-      if (a.fp) v = v - (*a.fbeta) * a.fp[r];
-      a.x[r] = v;
-      flag_nonfinite(a.st, v, a.step);
-    }
-    __syncthreads();
-  }
-
-  // one sweep over the slab: optional update with c, then dot or norm
-  auto sweep = [&](bool update, bool dot) {
-    if (dot)
-      for (int j = threadIdx.x; j < a.ncols; j += kThreads) colacc[j] = 0.0;
-    double nsum = 0.0;
-    __syncthreads();
-    for (int64_t r0 = s0; r0 < s1; r0 += CH) {
-      double xv[RPL];
-#pragma unroll
-      for (int e = 0; e < RPL; ++e) {
-        const int64_t r = r0 + lane + 32 * e;
-        xv[e] = r < s1 ? a.x[r] : 0.0;
-      }
-      if (update) {
-        double t[RPL];
-#pragma unroll
-        for (int e = 0; e < RPL; ++e) t[e] = 0.0;
-#pragma unroll 4
-        for (int j = warp; j < a.ncols; j += kWarps) {
-          const double cj = __ldcg(a.c + j);
-          const double* col = a.B + (int64_t)j * a.ldb;
-#pragma unroll
-          for (int e = 0; e < RPL; ++e) {
-            const int64_t r = r0 + lane + 32 * e;
-            if (r < s1) t[e] = fma(col[r], cj, t[e]);
-          }
-        }
-#pragma unroll
-        for (int e = 0; e < RPL; ++e) tred[warp][lane + 32 * e] = t[e];
-        __syncthreads();
-#pragma unroll
-        for (int e = 0; e < RPL; ++e) {
-          double s = tred[0][lane + 32 * e];
-#pragma unroll
-          for (int w = 1; w < kWarps; ++w) s += tred[w][lane + 32 * e];
-          xv[e] = xv[e] - s;
-          const int64_t r = r0 + lane + 32 * e;
-          if (warp == 0 && r < s1) a.x[r] = xv[e];
-        }
-        __syncthreads();
-      }
-      if (dot) {
-        // owned columns j = warp + 8q, in batches of 8
-        for (int q0 = 0; warp + kWarps * q0 < a.ncols; q0 += 8) {
-          double v[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int j = warp + kWarps * (q0 + u);
-            v[u] = 0.0;
-            if (j < a.ncols) {
-              const double* col = a.B + (int64_t)j * a.ldb;
-#pragma unroll
-              for (int e = 0; e < RPL; ++e) {
-                const int64_t r = r0 + lane + 32 * e;
-                if (r < s1) v[u] = fma(col[r], xv[e], v[u]);
-              }
-            }
-          }
-          const double t = warp_sum8(v);
-          const int j = warp + kWarps * (q0 + warp_sum8_index(lane));
-          if ((lane & 3) == 0 && j < a.ncols) colacc[j] += t;
-        }
-      } else if (warp == 0) {
-        double s = 0.0;
-#pragma unroll
-        for (int e = 0; e < RPL; ++e) s = fma(xv[e], xv[e], s);
-        nsum += warp_sum(s);
-      }
-    }
-    __syncthreads();
-    if (dot) {
-      for (int j = threadIdx.x; j < a.ncols; j += kThreads)
-        a.part[(int64_t)j * G + blockIdx.x] = colacc[j];
-    } else if (threadIdx.x == 0) {
-      a.part[blockIdx.x] = nsum;
-    }
-  };
-
-  if (a.ncols == 0 || a.passes == 0) {
-    sweep(false, false);
-  } else {
-    sweep(false, true);
-    for (int pass = 1; pass <= a.passes; ++pass) {
-      grid_barrier(a, G, bk);
-      coop_reduce_cols(a.part, a.ncols, (int)G, a.c);
-      grid_barrier(a, G, bk);
-      sweep(true, pass < a.passes);
-    }
-  }
-  grid_barrier(a, G, bk);
-  if (blockIdx.x == 0) {
-    // [4] norm test (k_norm_test semantics, incl. the host progress word)
-    double s = 0.0;
-    for (unsigned b = threadIdx.x; b < G; b += kThreads) s += __ldcg(a.part + b);
-    s = block_sum(s, tred[0]);
-    if (threadIdx.x == 0) nacc = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const double nrm = sqrt(nacc);
-      *a.slot = nrm;
-      int stop = ST_RUNNING;
-      if (a.st->nonfinite || !isfinite(nrm)) stop = ST_NONFINITE;
-      else if (nrm < a.eps) stop = a.code;
-      if (stop != ST_RUNNING) {
-        a.st->status = stop;
-        a.st->kprime = a.step;
-        a.st->where = a.step;
-      }
-      host_progress(a.hp, stop, a.step, a.side);
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Tile-resident fused CGS2 (single rank): as k_cgs2_coop, but each CTA first
-// pulls its whole basis tile (rows_per_cta x ncols) from L2/HBM into shared
-// memory with one bulk-async (TMA) copy per column segment, all in flight on
-// one mbarrier, then runs every sweep of the two CGS passes out of shared
-// memory.  The basis is read from memory once per orthogonalisation instead
-// of three times, and at full bulk-copy bandwidth instead of latency-bound
-// warp loads.  Used when the tile fits in shared memory (small / medium
-// bases: the L2-resident regime where CGS is latency-bound).
-template <int MAXE>
-__global__ void __launch_bounds__(kThreads, 1)
-k_cgs2_tile(CgsCoopArgs a) {
-  unsigned long long t_entry = 0;
-  if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0)
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_entry));
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ double tred[kWarps][32 * MAXE];
-  __shared__ __align__(8) unsigned long long mbar;
-  __shared__ double nacc;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned G = gridDim.x;
-  unsigned long long bk = 0;  // grid barriers passed in this launch
-  const int64_t s0 = (int64_t)blockIdx.x * a.rows_per_cta;
-  const int64_t s1 = min(a.L, s0 + a.rows_per_cta);
-  const int nr = s1 > s0 ? (int)(s1 - s0) : 0;
-  const int ldt = (nr + 1) & ~1;  // 16-byte column segments
-  double* tile = reinterpret_cast<double*>(smem_raw);
-  double* cs = tile + (size_t)a.ncols * ldt;  // coefficients of the current pass
-  const uint32_t bar = smem_u32(&mbar);
-
-  // bulk-async load of the basis tile: lane 0 of warp 0 arms the mbarrier
-  // with the total byte count, then the 32 lanes of warp 0 issue the
-  // per-column copies (one thread issuing ~100+ copies serially was the
-  // largest fixed cost of this kernel); all threads wait later.
-  if (warp == 0) {
-    const uint32_t bytes = (uint32_t)ldt * 8u;
-    if (lane == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      const uint32_t total = bytes * (uint32_t)a.ncols;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                   "r"(total)
-                   : "memory");
-    }
-    __syncwarp();
-    if (bytes)
-      for (int j = lane; j < a.ncols; j += 32) {
-        const double* src = a.B + (int64_t)j * a.ldb + s0;
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
-            "[%3];" ::"r"(smem_u32(tile + (size_t)j * ldt)),
-            "l"(src), "r"(bytes), "r"(bar)
-            : "memory");
-      }
-  }
-  // The basis columns were written >= 2 launches back (complete once the
-  // predecessor passed its own pdl_wait), so the tile copy above may run
-  // ahead of this wait; the partial sums / x below may not.
-  pdl_wait();
-  pdl_trigger(2);
-  if (halted(a.st)) {  // drain the copy into this CTA's smem before exiting
-    if (threadIdx.x == 0)
-      while (!mbar_try_wait(bar, 0)) {
-      }
-    return;
-  }
-  // [0] finalisation of the split partial sums of A^T q (overlaps the copy)
-  if (a.fpart) {
-    for (int64_t r = s0 + threadIdx.x; r < s1; r += kThreads) {
-      double v = strided_sum(a.fpart + r, a.fld, a.fnsplit);
-      if (a.fp) v = v - (*a.fbeta) * a.fp[r];
-      a.x[r] = v;
-      flag_nonfinite(a.st, v, a.step);
-    }
-  }
-  unsigned long long tl = 0;
-  phase_mark(a.tdbg, 0, tl);
-  if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(a.tdbg + 5, tl - t_entry);
-  __syncthreads();
-  // x rows of this CTA live in registers for the whole kernel (loaded while
-  // the tile is in flight)
-  double xv[MAXE];
-#pragma unroll
-  for (int e = 0; e < MAXE; ++e) {
-    const int rl = lane + 32 * e;
-    xv[e] = rl < nr ? a.x[s0 + rl] : 0.0;
-  }
-  while (!mbar_try_wait(bar, 0)) {
-  }
-  phase_mark(a.tdbg, 1, tl);  // [1] bulk copy of the tile (+ finalisation)
-
-  auto sweep = [&](bool update, bool dot) {
-    if (update) {
-      for (int j = threadIdx.x; j < a.ncols; j += kThreads) cs[j] = __ldcg(a.c + j);
-      __syncthreads();
-      double t[MAXE];
-#pragma unroll
-      for (int e = 0; e < MAXE; ++e) t[e] = 0.0;
-#pragma unroll 4
-      for (int j = warp; j < a.ncols; j += kWarps) {
-        const double cj = cs[j];
-        const double* col = tile + (size_t)j * ldt;
-#pragma unroll
-        for (int e = 0; e < MAXE; ++e) {
-          const int rl = lane + 32 * e;
-          if (rl < nr) t[e] = fma(col[rl], cj, t[e]);
-        }
-      }
-#pragma unroll
-      for (int e = 0; e < MAXE; ++e) tred[warp][lane + 32 * e] = t[e];
-      __syncthreads();
-#pragma unroll
-      for (int e = 0; e < MAXE; ++e) {
-        double s = tred[0][lane + 32 * e];
-#pragma unroll
-        for (int w = 1; w < kWarps; ++w) s += tred[w][lane + 32 * e];
-        xv[e] = xv[e] - s;
-        const int rl = lane + 32 * e;
-        if (!dot && warp == 0 && rl < nr) a.x[s0 + rl] = xv[e];  // final pass only
-      }
-      __syncthreads();
-    }
-    if (dot) {
-      for (int q0 = 0; warp + kWarps * q0 < a.ncols; q0 += 8) {
-        double v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int j = warp + kWarps * (q0 + u);
-          v[u] = 0.0;
-          if (j < a.ncols) {
-            const double* col = tile + (size_t)j * ldt;
-#pragma unroll
-            for (int e = 0; e < MAXE; ++e) {
-              const int rl = lane + 32 * e;
-              if (rl < nr) v[u] = fma(col[rl], xv[e], v[u]);
-            }
-          }
-        }
-        const double t = warp_sum8(v);
-        const int j = warp + kWarps * (q0 + warp_sum8_index(lane));
-        if ((lane & 3) == 0 && j < a.ncols) a.part[(int64_t)j * G + blockIdx.x] = t;
-      }
-    } else if (warp == 0) {
-      double s = 0.0;
-#pragma unroll
-      for (int e = 0; e < MAXE; ++e) s = fma(xv[e], xv[e], s);
-      s = warp_sum(s);
-      if (lane == 0) a.part[blockIdx.x] = s;
-    }
-  };
-
-  if (a.ncols == 0 || a.passes == 0) {
-    sweep(false, false);
-    phase_mark(a.tdbg, 2, tl);
-  } else {
-    sweep(false, true);
-    phase_mark(a.tdbg, 2, tl);  // [2] sweeps
-    for (int pass = 1; pass <= a.passes; ++pass) {
-      grid_barrier(a, G, bk);
-      phase_mark(a.tdbg, 3, tl);  // [3] barriers
-      coop_reduce_cols(a.part, a.ncols, (int)G, a.c);
-      phase_mark(a.tdbg, 4, tl);  // [4] reductions
-      grid_barrier(a, G, bk);
-      phase_mark(a.tdbg, 3, tl);
-      sweep(true, pass < a.passes);
-      phase_mark(a.tdbg, 2, tl);
-    }
-  }
-  grid_barrier(a, G, bk);
-  phase_mark(a.tdbg, 3, tl);
-  if (blockIdx.x == 0) {
-    double s = 0.0;
-    for (unsigned b = threadIdx.x; b < G; b += kThreads) s += __ldcg(a.part + b);
-    s = block_sum(s, tred[0]);
-    if (threadIdx.x == 0) nacc = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const double nrm = sqrt(nacc);
-      *a.slot = nrm;
-      int stop = ST_RUNNING;
-      if (a.st->nonfinite || !isfinite(nrm)) stop = ST_NONFINITE;
-      else if (nrm < a.eps) stop = a.code;
-      if (stop != ST_RUNNING) {
-        a.st->status = stop;
-        a.st->kprime = a.step;
-        a.st->where = a.step;
-      }
-      host_progress(a.hp, stop, a.step, a.side);
-    }
-  }
-  if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0) {
-    unsigned long long now;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-    atomicAdd(a.tdbg + 6, now - t_entry);
-    atomicAdd(a.tdbg + 7, 1ull);
-  }
-}
-
-
-// Same work as k_cgs2_tile with 2 grid-wide rounds per CGS2 instead of 5:
-// every CTA reduces all G partials of every column itself (a few KB-170 KB
-// of L2 reads, cheaper than a second barrier), the partial buffers
-// ping-pong between passes, and beta^2 = ||x||^2 - ||c||^2 comes with the
-// last pass's dot products (direct-norm round only when that would cancel).
-// k_cgs2_tile2 in two device functions, so the persistent streaming kernel
-// (stream.cuh) runs the same CGS2 inside its step loop: tile2_issue starts
-// the bulk copy of this CTA's basis tile, tile2_rest does the rest.  Every
-// load of data another CTA may have written in the same launch goes through
-// L2 (__ldcg / volatile), and the tile copy is fenced against the generic
-// proxy (fence.proxy.async) -- needed once the kernel is persistent.
+// Tile-resident fused CGS2 (k_cgs2_tile2): each CTA first pulls its whole
+// basis tile (rows_per_cta x ncols) from L2/HBM into shared memory with one
+// bulk-async (TMA) copy per column segment, all in flight on one mbarrier,
+// then runs every sweep of the two CGS passes out of shared memory -- the
+// basis is read once per orthogonalisation, at bulk-copy bandwidth.  2 grid
+// rounds per CGS2 where every CTA reduces all G partials of every column
+// itself (a few KB of L2 reads, cheaper than a second barrier), else 4
+// (distributed column sums + a barrier); the partial buffers ping-pong
+// between passes, and beta^2 = ||x||^2 - ||c||^2 comes with the last pass's
+// dot products (direct-norm round only when that would cancel).  tile2_issue
+// starts the bulk copy of this CTA's tile, tile2_rest does the rest.  Every
+// load of data another CTA wrote in the same launch goes through L2
+// (__ldcg / volatile), and the tile copy is fenced against the generic
+// proxy (fence.proxy.async).
 __device__ __forceinline__ void tile2_issue(const CgsCoopArgs& a, double* tile, uint32_t bar,
                                             bool init) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

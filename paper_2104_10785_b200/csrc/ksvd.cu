@@ -14,6 +14,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <map>
+#include <mutex>
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -30,7 +32,6 @@
 #include "klrm.cuh"
 #include "resident.cuh"
 #include "peer.cuh"
-#include "stream.cuh"
 #include "ksvd.h"
 
 using namespace ksvd;
@@ -74,6 +75,21 @@ int ksvd_set_error_from_host(int code, const char* msg) { return set_err(code, "
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 static inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize applies per device: set it
+// once per (kernel, device) -- a context on a second GPU of the process gets
+// its own -- and check the return code.
+static int smem_attr(const void* kern, int device, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(kern, device);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return 0;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done[key] = bytes;
+  return 0;
+}
+
 // ---------------------------------------------------------------------------
 // context
 enum KClass {
@@ -114,6 +130,9 @@ struct ksvd_ctx {
   void* stage[2] = {nullptr, nullptr};
   size_t stage_bytes = 0;
   cudaEvent_t stage_ev[2] = {};
+  // grid-barrier kernels: regular launches (all CTAs resident, probed at
+  // creation) or, where residency is not guaranteed, cooperative launches
+  bool coop_cgs = false;
 };
 
 static int get_event(ksvd_ctx* c, cudaEvent_t* ev) {
@@ -482,7 +501,7 @@ static int dense_gemv_t(ksvd_mat* M, const double* q_src, const double* q_scale,
   }
   const int nsplit = M->mloc > 0 ? (int)pt.nsplit : 1;
   const bool multi = c->comm != nullptr;
-  if (!finalize && !multi) return 0;  // fused into the caller's k_cgs2_coop
+  if (!finalize && !multi) return 0;  // fused into the caller's k_cgs2_tile2
   if (multi && c->px && M->n_pad <= c->px_slot) {
     // split sums + peer exchange + (- beta p) + check in one kernel
     int64_t G = 1;
@@ -510,7 +529,7 @@ static int dense_gemv_t(ksvd_mat* M, const double* q_src, const double* q_scale,
   return 0;
 }
 
-struct FinArgs {  // deferred gemv_t finalisation (phase 0 of k_cgs2_coop)
+struct FinArgs {  // deferred gemv_t finalisation (phase 0 of k_cgs2_tile2)
   const double* part = nullptr;
   int64_t ld = 0;
   int nsplit = 0;
@@ -593,8 +612,6 @@ struct CgsWork {
   double* c = nullptr;     // cap
   double* red = nullptr;   // 2
   unsigned* bar = nullptr; // grid barrier {count, generation}
-  unsigned long long* flags = nullptr;  // flag barrier: 256 lines of 128 bytes
-  unsigned long long epoch = 0;         // last target issued (16 per launch)
   int64_t part_elems = 0;
   int cap = 0;
 };
@@ -627,10 +644,6 @@ static int ensure_cgs(cudaStream_t s, CgsWork* w, int64_t nrb, int cols) {
   if (!w->bar) {
     CK(cudaMallocAsync((void**)&w->bar, sizeof(unsigned) * 2, s));
     CK(cudaMemsetAsync(w->bar, 0, sizeof(unsigned) * 2, s));
-  }
-  if (!w->flags) {
-    CK(cudaMallocAsync((void**)&w->flags, 256 * 128, s));
-    CK(cudaMemsetAsync(w->flags, 0, 256 * 128, s));
   }
   return 0;
 }
@@ -676,72 +689,31 @@ static int cgs_impl(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int n
   return 0;
 }
 
-// ---- single-rank fused CGS2 (k_cgs2_coop) ----
-constexpr int kCoopRPL = 4;
-constexpr int kCoopMaxCols = 12288;  // colacc in dynamic shared memory (96 KB)
+// ---- single-rank fused CGS2 (k_cgs2_tile2) ----
+constexpr size_t kTileSmemMax = 200 * 1024;  // basis tile budget of k_cgs2_tile2
 
-
-constexpr size_t kTileSmemMax = 200 * 1024;  // basis tile budget of k_cgs2_tile
-
-// Fused single-kernel CGS2 is used where its basis tile fits in shared
+// The fused single-kernel CGS2 is used where its basis tile fits in shared
 // memory (one CTA per SM): there it beats the multi-kernel path by its
 // launches; for long vectors (configs 3-5, left side) the multi-kernel path
-// with ~L/128 CTAs streams the basis faster than a one-wave cooperative grid
-// (measured: config 3 581 vs 600 ms per call).  KSVD_COOP=0 disables the
-// fused path, KSVD_COOP_GLOBAL=1 also uses the streaming cooperative kernel.
+// with ~L/128 CTAs streams the basis (measured: a one-wave cooperative grid
+// streaming it from L2/HBM was slower, config 3 600 vs 581 ms per call).
+// KSVD_COOP=0 forces the multi-kernel path (tests).
 static bool coop_enabled(const ksvd_ctx* c, int64_t L, int ncols, bool sharded) {
   static const bool off = [] {
     const char* e = getenv("KSVD_COOP");
     return e && strcmp(e, "0") == 0;
   }();
-  static const bool global = [] {
-    const char* e = getenv("KSVD_COOP_GLOBAL");
-    return e && strcmp(e, "1") == 0;
-  }();
   // a sharded basis needs all-reduces between the passes (multi-kernel path);
   // the replicated right basis takes the fused kernel at any rank count
-  if (off || (sharded && c->comm != nullptr) || ncols > kCoopMaxCols) return false;
+  if (off || (sharded && c->comm != nullptr)) return false;
   const int64_t G = std::min<int64_t>(c->sms, std::max<int64_t>(1, cdiv(L, 32)));
   const int64_t rows = rup(cdiv(std::max<int64_t>(L, 1), G), 2);
-  const bool tile =
-      rows <= 256 && sizeof(double) * (size_t)ncols * (size_t)(rows + 1) + 16 <= kTileSmemMax;
-  return tile || global;
-}
-
-static int coop_max_ctas(ksvd_ctx* c) {
-  static int per_sm = -1;
-  if (per_sm < 0) {
-    auto k = k_cgs2_coop<kCoopRPL>;
-    const int smem = kCoopMaxCols * (int)sizeof(double);
-    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, smem));
-    per_sm = std::max(1, std::min(occ, 2));
-  }
-  return per_sm * c->sms;
+  return rows <= 256 && sizeof(double) * (size_t)ncols * (size_t)(rows + 1) + 16 <= kTileSmemMax;
 }
 
 template <int MAXE>
-static int tile_attr() {
-  static bool done = false;
-  if (!done) {
-    CK(cudaFuncSetAttribute(k_cgs2_tile<MAXE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)kTileSmemMax));
-    CK(cudaFuncSetAttribute(k_cgs2_tile2<MAXE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)kTileSmemMax));
-    done = true;
-  }
-  return 0;
-}
-
-// k_cgs2_tile2 (2 grid rounds per CGS2) unless KSVD_CGS_SYNC=5 selects the
-// 5-round k_cgs2_tile (A/B)
-static bool tile2_enabled() {
-  static const bool v = [] {
-    const char* e = getenv("KSVD_CGS_SYNC");
-    return !(e && strcmp(e, "5") == 0);
-  }();
-  return v;
+static int tile_attr(int device) {
+  return smem_attr((const void*)k_cgs2_tile2<MAXE>, device, (int)kTileSmemMax);
 }
 
 static int cgs_coop(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int ncols, double* x,
@@ -783,38 +755,27 @@ static int cgs_coop(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int n
   const size_t tile_bytes = sizeof(double) * (size_t)ncols * (size_t)(rows + 1);
   const void* kern = nullptr;
   size_t smem = 0;
-  static const bool tile_off = [] {
-    const char* e = getenv("KSVD_TILE");
-    return e && strcmp(e, "0") == 0;
-  }();
-  const bool t2 = tile2_enabled();
-  if (!tile_off && rows <= 256 && tile_bytes + 16 <= kTileSmemMax) {
-    smem = tile_bytes + 16;  // + the (ncols + 1)-th reduced sum of k_cgs2_tile2
-    switch ((int)cdiv(rows, 32)) {
-#define KSVD_TILE_CASE(E)                                                      \
-  case E:                                                                      \
-    TRY(tile_attr<E>());                                                       \
-    kern = t2 ? (const void*)k_cgs2_tile2<E> : (const void*)k_cgs2_tile<E>;    \
+  if (!(rows <= 256 && tile_bytes + 16 <= kTileSmemMax))
+    return set_err(KSVD_ERUNTIME, "internal: CGS2 tile of %lld rows x %d columns does not fit",
+                   (long long)rows, ncols);
+  smem = tile_bytes + 16;  // + the (ncols + 1)-th reduced sum
+  switch ((int)cdiv(rows, 32)) {
+#define KSVD_TILE_CASE(E)                  \
+  case E:                                  \
+    TRY(tile_attr<E>(c->device));          \
+    kern = (const void*)k_cgs2_tile2<E>;   \
     break;
-      KSVD_TILE_CASE(1)
-      KSVD_TILE_CASE(2)
-      KSVD_TILE_CASE(3)
-      KSVD_TILE_CASE(4)
-      KSVD_TILE_CASE(5)
-      KSVD_TILE_CASE(6)
-      KSVD_TILE_CASE(7)
-      default:
-        TRY(tile_attr<8>());
-        kern = t2 ? (const void*)k_cgs2_tile2<8> : (const void*)k_cgs2_tile<8>;
+    KSVD_TILE_CASE(1)
+    KSVD_TILE_CASE(2)
+    KSVD_TILE_CASE(3)
+    KSVD_TILE_CASE(4)
+    KSVD_TILE_CASE(5)
+    KSVD_TILE_CASE(6)
+    KSVD_TILE_CASE(7)
+    default:
+      TRY(tile_attr<8>(c->device));
+      kern = (const void*)k_cgs2_tile2<8>;
 #undef KSVD_TILE_CASE
-    }
-  } else {
-    constexpr int CH = 32 * kCoopRPL;
-    G = std::min<int64_t>(coop_max_ctas(c), std::max<int64_t>(1, cdiv(L, CH)));
-    rows = rup(cdiv(std::max<int64_t>(L, 1), G), 32);
-    G = std::max<int64_t>(1, cdiv(L, rows));
-    smem = sizeof(double) * std::max(ncols, 1);
-    kern = (const void*)k_cgs2_coop<kCoopRPL>;
   }
   a.rows_per_cta = (int)rows;
   // k_cgs2_tile2 reduction mode: every CTA reads all G x (ncols + 1) partials
@@ -835,32 +796,16 @@ static int cgs_coop(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int n
     CK(cudaEventRecord(e0, c->stream));
   }
   {
-    // A regular launch with the flip barrier of grid_barrier (default), so
+    // A regular launch with the flip barrier of grid_barrier, so
     // programmatic dependent launch starts the grid while the product
     // drains: its CTAs are scheduled only once every CTA of the product has
     // started, and all G <= #SMs of them are resident once the product's
     // CTAs retire (one CTA per SM).  Measured on config 2: 3692 vs 3624 GK
-    // steps/s for the cooperative launch (KSVD_COOP_LAUNCH=1), whose ~6 us
-    // launch cannot overlap the product's tail.
-    static const bool regular = [] {
-      const char* e = getenv("KSVD_COOP_LAUNCH");
-      return !(e && strcmp(e, "1") == 0);
-    }();
-    const bool reg = regular && G <= c->sms;
+    // steps/s for a cooperative launch, whose ~6 us launch cannot overlap
+    // the product's tail -- which stays the fallback where residency is not
+    // guaranteed (ctx->coop_cgs, see residency_probe).
+    const bool reg = !c->coop_cgs && G <= c->sms;
     if (!reg) a.bar = nullptr;
-    // KSVD_FLAG_BARRIER=1 (experiment): per-CTA flag lines polled by every
-    // CTA instead of the flip barrier's single word.  Measured on config 2:
-    // 3.8 vs 3.15 us of barrier time per CGS launch (the 148 x 148 polls
-    // contend in L2), 3698 vs 3733 GK steps/s -- so off by default.
-    static const bool flag_bar = [] {
-      const char* e = getenv("KSVD_FLAG_BARRIER");
-      return e && strcmp(e, "1") == 0;
-    }();
-    if (reg && flag_bar && G <= kThreads) {
-      a.flags = W->flags;
-      a.epoch = W->epoch;
-      W->epoch += 16;  // <= 5 barriers per CGS launch
-    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)G);
     cfg.blockDim = dim3(kThreads);
@@ -938,14 +883,9 @@ static bool multi_tile_enabled(const ksvd_ctx* c, int64_t L, int ncols) {
 }
 
 template <int E>
-static const void* phase_kernel() {
-  static bool done = false;
-  if (!done) {
-    cudaFuncSetAttribute(k_cgs_tile_phase<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kTileSmemMax);
-    done = true;
-  }
-  return (const void*)k_cgs_tile_phase<E>;
+static const void* phase_kernel(int device) {
+  const void* k = (const void*)k_cgs_tile_phase<E>;
+  return smem_attr(k, device, (int)kTileSmemMax) == 0 ? k : nullptr;
 }
 
 static int cgs_tile_multi(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb, int ncols,
@@ -955,15 +895,16 @@ static int cgs_tile_multi(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb,
   const TileGeom g = tile_geom(c, L, ncols);
   const void* kern = nullptr;
   switch ((int)cdiv(g.rows, 32)) {
-    case 1: kern = phase_kernel<1>(); break;
-    case 2: kern = phase_kernel<2>(); break;
-    case 3: kern = phase_kernel<3>(); break;
-    case 4: kern = phase_kernel<4>(); break;
-    case 5: kern = phase_kernel<5>(); break;
-    case 6: kern = phase_kernel<6>(); break;
-    case 7: kern = phase_kernel<7>(); break;
-    default: kern = phase_kernel<8>(); break;
+    case 1: kern = phase_kernel<1>(c->device); break;
+    case 2: kern = phase_kernel<2>(c->device); break;
+    case 3: kern = phase_kernel<3>(c->device); break;
+    case 4: kern = phase_kernel<4>(c->device); break;
+    case 5: kern = phase_kernel<5>(c->device); break;
+    case 6: kern = phase_kernel<6>(c->device); break;
+    case 7: kern = phase_kernel<7>(c->device); break;
+    default: kern = phase_kernel<8>(c->device); break;
   }
+  if (!kern) return set_err(KSVD_ERUNTIME, "k_cgs_tile_phase: shared-memory attribute");
   TRY(ensure_cgs(c->stream, W, g.G, 2 * (ncols + 1)));
   CgsCoopArgs a{};
   a.B = B;
@@ -976,7 +917,9 @@ static int cgs_tile_multi(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb,
   a.step = step;
   a.part = W->part;
   a.c = W->c;
-  a.bar = W->bar;  // regular launch, flip barrier (one CTA per SM, G <= #SMs)
+  // regular launch with the flip barrier (one CTA per SM, G <= #SMs), or a
+  // cooperative launch where residency is not guaranteed (ctx->coop_cgs)
+  a.bar = c->coop_cgs ? nullptr : W->bar;
   a.tdbg = nullptr;
   const int phases[3] = {0, 1, 2};
   for (int k = 0; k < 3; ++k) {
@@ -1003,11 +946,20 @@ static int cgs_tile_multi(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb,
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = g.smem;
     cfg.stream = c->stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (c->coop_cgs) {
+      at[na].id = cudaLaunchAttributeCooperative;
+      at[na].val.cooperative = 1;
+      ++na;
+    }
+    if (pdl_enabled(c)) {
+      at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[na].val.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled(c) ? 1 : 0;
+    cfg.numAttrs = na;
     CK(cudaLaunchKernelExC(&cfg, kern, args));
     if (c->profiling) {
       CK(cudaEventRecord(e1, c->stream));
@@ -1076,8 +1028,7 @@ static void free_run(ksvd_run* R) {
                   (void*)R->beta, (void*)R->slot, (void*)R->G, (void*)R->V, (void*)R->U,
                   (void*)R->sig, (void*)R->left.part, (void*)R->left.c, (void*)R->left.red,
                   (void*)R->left.bar, (void*)R->right.part, (void*)R->right.c,
-                  (void*)R->right.red, (void*)R->right.bar, (void*)R->left.flags,
-                  (void*)R->right.flags, (void*)R->st, (void*)R->st_aux})
+                  (void*)R->right.red, (void*)R->right.bar, (void*)R->st, (void*)R->st_aux})
     if (p) cudaFreeAsync(p, c->stream);
   delete R;
 }
@@ -1200,327 +1151,12 @@ static int read_state(ksvd_run* R) {
   return 0;
 }
 
-// L2 residency for A across the two passes of a GK step, as a persisting
-// access-policy window over a slice of A.  Measured slower on B200 for
-// config 2 (gemv 124 us vs 116 us: the set-aside shrinks the L2 the band
-// sweep of k_gemv_n2 / k_gemv_t already reuses), so it is opt-in
-// (KSVD_L2_PERSIST=1).
-static int set_l2_window(ksvd_mat* M, bool on) {
-  ksvd_ctx* c = M->ctx;
-  static const bool off = [] {
-    const char* e = getenv("KSVD_L2_PERSIST");
-    return !(e && strcmp(e, "1") == 0);
-  }();
-  if (off) return 0;
-  int max_persist = 0, max_window = 0;
-  CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device));
-  CK(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, c->device));
-  const size_t abytes = M->A ? (size_t)M->mloc * M->lda * esize(M->dtype) : 0;
-  if (max_persist <= 0 || max_window <= 0 || abytes == 0) return 0;
-  cudaStreamAttrValue v{};
-  if (on) {
-    CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist));
-    const size_t win = std::min<size_t>(abytes, (size_t)max_window);
-    v.accessPolicyWindow.base_ptr = M->A;
-    v.accessPolicyWindow.num_bytes = win;
-    v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)max_persist / (double)win);
-    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-  } else {
-    v.accessPolicyWindow.num_bytes = 0;
-  }
-  CK(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v));
-  if (!on) CK(cudaCtxResetPersistingL2Cache());
-  return 0;
-}
-
 static int run_steps(ksvd_run* R, int i0);
-
-// ---------------------------------------------------------------------------
-// Persistent streaming kernel (stream.cuh): single rank, f64, the gemv_n
-// plan at one CTA per SM, a gemv_t plan with 8 row groups; runs steps
-// 1..i_end where both CGS2 basis tiles still fit shared memory, then (if the
-// run has not stopped) the 4-launch loop continues at i_end + 1.
-// Opt-in (KSVD_STREAM=1): measured on config 2 (CTA-0 phase times per step)
-// the two CGS2 phases drop from ~48 to ~39 us, but A^T q at one CTA per SM
-// takes 152 us against 117 us for the standalone k_gemv_t2 at four CTAs per
-// SM (loads in flight), so the 4-launch loop stays the default.
-static bool stream_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("KSVD_STREAM");
-    return e && strcmp(e, "1") == 0;
-  }();
-  return on;
-}
-
-static size_t tile_bytes_for(int64_t rows, int ncols) {
-  const int64_t ldt = (rows + 1) & ~(int64_t)1;
-  return sizeof(double) * ((size_t)ncols * ldt + ncols + 2) + 16;
-}
-
-template <int MAXE, int ITT>
-static int stream_attr(size_t smem) {
-  CK(cudaFuncSetAttribute(k_gk_stream<MAXE, ITT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)smem));
-  return 0;
-}
-
-static int run_stream(ksvd_run* R, int* i0) {
-  ksvd_mat* M = R->M;
-  ksvd_ctx* c = M->ctx;
-  if (!stream_enabled() || c->comm || M->fac || M->dtype != KSVD_F64 || M->mloc == 0)
-    return 0;
-  const int64_t G = c->sms;
-  if (M->pn.blocks > G || M->pt.rg != 8) return 0;
-  const int64_t rows_l = rup(cdiv(M->mloc, G), 2), rows_r = rup(cdiv(M->n, G), 2);
-  if (rows_l > 256 || rows_r > 256) return 0;
-  // dynamic tile budget: leave room for the kernel's static shared memory
-  // (CGS row sums, gemv_t q staging and group sums: <= 28 KB) under 227 KB
-  constexpr size_t kStreamTileMax = kTileSmemMax - 32 * 1024;
-  int i_end = 0;
-  for (int i = 1; i <= R->k_max; ++i) {
-    if (tile_bytes_for(rows_l, i) > kStreamTileMax || tile_bytes_for(rows_r, i) > kStreamTileMax)
-      break;
-    i_end = i;
-  }
-  if (i_end < 8) return 0;  // too few steps to be worth a launch
-  const size_t smem = std::max(tile_bytes_for(rows_l, i_end), tile_bytes_for(rows_r, i_end));
-  TRY(grow_bases(R, i_end + 1 <= R->k_max ? i_end + 1 : i_end));
-  TRY(ensure_cgs(c->stream, &R->left, G, 2 * (i_end + 2)));
-  TRY(ensure_cgs(c->stream, &R->right, G, 2 * (i_end + 2)));
-  static const int64_t red_max = [] {
-    const char* e = getenv("KSVD_RED_MAX");
-    return e ? (int64_t)atoll(e) : (int64_t)148 * 16;
-  }();
-  StreamArgs a{};
-  a.A = (const double*)M->A;
-  a.lda = M->lda;
-  a.mloc = M->mloc;
-  a.n = M->n;
-  a.nvec = M->pn.nvec;
-  a.nchunks = M->pn.nchunks;
-  a.nseg = M->pn.rows_per_warp;
-  a.part_n = M->part_n;
-  a.ncoltiles = M->pt.ncoltiles;
-  a.nsplit = M->pt.nsplit;
-  a.ldz = M->n_pad;
-  a.part_t = M->part_t;
-  a.Q = R->Q;
-  a.P = R->P;
-  a.ldq = R->ldq;
-  a.ldp = R->ldp;
-  a.w = R->w;
-  a.z = R->z;
-  a.alpha = R->alpha;
-  a.beta = R->beta;
-  a.st = R->st;
-  a.i0 = 1;
-  a.i_end = i_end;
-  a.k_max = R->k_max;
-  a.passes = R->reorth;
-  a.eps = R->eps;
-  a.rows_l = (int)rows_l;
-  a.rows_r = (int)rows_r;
-  a.lpart = R->left.part;
-  a.lc = R->left.c;
-  a.lbar = R->left.bar;
-  a.rpart = R->right.part;
-  a.rc = R->right.c;
-  a.rbar = R->right.bar;
-  a.red_max = red_max;
-  a.hp = c->dprog;
-  a.tdbg = c->tdbg;
-  void* args[] = {&a};
-  const bool big = (size_t)M->mloc * M->lda * sizeof(double) >= ((size_t)2 << 30);
-  const int maxe = (int)cdiv(std::max(rows_l, rows_r), 32);
-  const void* kern = nullptr;
-#define KSVD_STREAM_CASE(E)                                                  \
-  case E:                                                                    \
-    if (big) {                                                               \
-      TRY((stream_attr<E, 8>(smem)));                                        \
-      kern = (const void*)k_gk_stream<E, 8>;                                 \
-    } else {                                                                 \
-      TRY((stream_attr<E, 2>(smem)));                                        \
-      kern = (const void*)k_gk_stream<E, 2>;                                 \
-    }                                                                        \
-    break;
-  switch (maxe) {
-    KSVD_STREAM_CASE(1)
-    KSVD_STREAM_CASE(2)
-    KSVD_STREAM_CASE(3)
-    KSVD_STREAM_CASE(4)
-    KSVD_STREAM_CASE(5)
-    KSVD_STREAM_CASE(6)
-    KSVD_STREAM_CASE(7)
-    default:
-      KSVD_STREAM_CASE(8)
-  }
-#undef KSVD_STREAM_CASE
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (c->profiling) {
-    TRY(get_event(c, &e0));
-    TRY(get_event(c, &e1));
-    CK(cudaEventRecord(e0, c->stream));
-  }
-  const cudaError_t e =
-      cudaLaunchCooperativeKernel(kern, dim3((unsigned)G), dim3(kThreads), args, smem, c->stream);
-  if (e != cudaSuccess)
-    return set_err(KSVD_ERUNTIME, "persistent GK launch: %s", cudaGetErrorString(e));
-  if (c->profiling) {
-    CK(cudaEventRecord(e1, c->stream));
-    c->pending.push_back({e0, e1, KC_RESIDENT});
-  }
-  c->launches++;
-  if (c->tdbg) {
-    unsigned long long t[8];
-    CK(cudaMemcpyAsync(t, c->tdbg, sizeof t, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    fprintf(stderr, "[ksvd] stream phases (us, CTA 0, cumulative): gemv_n %.1f cgs_left %.1f "
-            "gemv_t %.1f cgs_right %.1f\n", t[0] * 1e-3, t[1] * 1e-3, t[2] * 1e-3, t[3] * 1e-3);
-    CK(cudaMemsetAsync(c->tdbg, 0, sizeof t, c->stream));
-  }
-  // continue with the 4-launch loop only if the run is still going
-  DevState h{};
-  CK(cudaMemcpyAsync(&h, R->st, sizeof h, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  *i0 = (h.status == ST_RUNNING && i_end < R->k_max) ? i_end + 1 : R->k_max + 1;
-  return 0;
-}
-
-// Row-streamed persistent kernel (stream.cuh k_gk_rows): A's rows through a
-// bulk-copy ring in shared memory, 2 grid barriers per step besides the
-// CGS2 rounds.  KSVD_ROWS=1 enables it (single rank, f64, n <= 6144).
-static bool rows_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("KSVD_ROWS");
-    return e && strcmp(e, "1") == 0;
-  }();
-  return on;
-}
-
-template <int MAXE>
-static int rows_attr(size_t smem) {
-  CK(cudaFuncSetAttribute(k_gk_rows<MAXE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)smem));
-  return 0;
-}
-
-static int run_rows(ksvd_run* R, int* i0) {
-  ksvd_mat* M = R->M;
-  ksvd_ctx* c = M->ctx;
-  if (!rows_enabled() || c->comm || M->fac || M->dtype != KSVD_F64 || M->mloc == 0) return 0;
-  const int64_t G = c->sms;
-  if (M->n > (int64_t)kThreads * kRowCols) return 0;
-  const int64_t rows_l = rup(cdiv(M->mloc, G), 2), rows_r = rup(cdiv(M->n, G), 2);
-  if (rows_l > 256 || rows_r > 256) return 0;
-  constexpr size_t kBudget = kTileSmemMax - 32 * 1024;  // + ~30 KB static
-  const size_t ring = sizeof(double) * kRowRing * (size_t)rup(M->n, 2);
-  if (ring > kBudget) return 0;
-  int i_end = 0;
-  for (int i = 1; i <= R->k_max; ++i) {
-    if (tile_bytes_for(rows_l, i) > kBudget || tile_bytes_for(rows_r, i) > kBudget) break;
-    i_end = i;
-  }
-  if (i_end < 8) return 0;
-  const size_t smem =
-      std::max({ring, tile_bytes_for(rows_l, i_end), tile_bytes_for(rows_r, i_end)});
-  TRY(grow_bases(R, i_end + 1 <= R->k_max ? i_end + 1 : i_end));
-  TRY(ensure_cgs(c->stream, &R->left, G, 2 * (i_end + 2)));
-  TRY(ensure_cgs(c->stream, &R->right, G, 2 * (i_end + 2)));
-  double* zpart = nullptr;
-  CK(cudaMallocAsync(&zpart, sizeof(double) * G * M->n_pad, c->stream));
-  static const int64_t red_max = [] {
-    const char* e = getenv("KSVD_RED_MAX");
-    return e ? (int64_t)atoll(e) : (int64_t)148 * 16;
-  }();
-  RowsArgs a{};
-  a.A = (const double*)M->A;
-  a.lda = M->lda;
-  a.mloc = M->mloc;
-  a.n = M->n;
-  a.ldz = M->n_pad;
-  a.Q = R->Q;
-  a.P = R->P;
-  a.ldq = R->ldq;
-  a.ldp = R->ldp;
-  a.w = R->w;
-  a.z = R->z;
-  a.alpha = R->alpha;
-  a.beta = R->beta;
-  a.zpart = zpart;
-  a.st = R->st;
-  a.i0 = 1;
-  a.i_end = i_end;
-  a.k_max = R->k_max;
-  a.passes = R->reorth;
-  a.eps = R->eps;
-  a.rows_l = (int)rows_l;
-  a.rows_r = (int)rows_r;
-  a.lpart = R->left.part;
-  a.lc = R->left.c;
-  a.lbar = R->left.bar;
-  a.rpart = R->right.part;
-  a.rc = R->right.c;
-  a.rbar = R->right.bar;
-  a.red_max = red_max;
-  a.hp = c->dprog;
-  a.tdbg = c->tdbg;
-  void* args[] = {&a};
-  const int maxe = (int)cdiv(std::max(rows_l, rows_r), 32);
-  const void* kern = nullptr;
-#define KSVD_ROWS_CASE(E)                      \
-  case E:                                      \
-    TRY(rows_attr<E>(smem));                   \
-    kern = (const void*)k_gk_rows<E>;          \
-    break;
-  switch (maxe) {
-    KSVD_ROWS_CASE(1)
-    KSVD_ROWS_CASE(2)
-    KSVD_ROWS_CASE(3)
-    KSVD_ROWS_CASE(4)
-    KSVD_ROWS_CASE(5)
-    KSVD_ROWS_CASE(6)
-    KSVD_ROWS_CASE(7)
-    default:
-      KSVD_ROWS_CASE(8)
-  }
-#undef KSVD_ROWS_CASE
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (c->profiling) {
-    TRY(get_event(c, &e0));
-    TRY(get_event(c, &e1));
-    CK(cudaEventRecord(e0, c->stream));
-  }
-  const cudaError_t e =
-      cudaLaunchCooperativeKernel(kern, dim3((unsigned)G), dim3(kThreads), args, smem, c->stream);
-  cudaFreeAsync(zpart, c->stream);
-  if (e != cudaSuccess)
-    return set_err(KSVD_ERUNTIME, "row-streamed GK launch: %s", cudaGetErrorString(e));
-  if (c->profiling) {
-    CK(cudaEventRecord(e1, c->stream));
-    c->pending.push_back({e0, e1, KC_RESIDENT});
-  }
-  c->launches++;
-  if (c->tdbg) {
-    unsigned long long t[8];
-    CK(cudaMemcpyAsync(t, c->tdbg, sizeof t, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    fprintf(stderr, "[ksvd] rows phases (us, CTA 0, cumulative): gemv_n %.1f cgs_left %.1f "
-            "gemv_t %.1f cgs_right %.1f\n", t[0] * 1e-3, t[1] * 1e-3, t[2] * 1e-3, t[3] * 1e-3);
-    CK(cudaMemsetAsync(c->tdbg, 0, sizeof t, c->stream));
-  }
-  DevState h{};
-  CK(cudaMemcpyAsync(&h, R->st, sizeof h, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  *i0 = (h.status == ST_RUNNING && i_end < R->k_max) ? i_end + 1 : R->k_max + 1;
-  return 0;
-}
 
 static int run_loop(ksvd_run* R, const double* q1_local) {
   ksvd_mat* M = R->M;
   ksvd_ctx* c = M->ctx;
   TRY(grow_bases(R, std::min(R->k_max, 64)));
-  TRY(set_l2_window(M, true));
   if (M->mloc > 0)
     CK(cudaMemcpyAsync(R->Q, q1_local, sizeof(double) * M->mloc, cudaMemcpyHostToDevice,
                        c->stream));
@@ -1528,26 +1164,19 @@ static int run_loop(ksvd_run* R, const double* q1_local) {
   TRY(enqueue_gemv_t(M, R->Q, nullptr, nullptr, nullptr, nullptr, R->z, R->st, 0, true));
   TRY(cgs(c, &R->right, R->P, R->ldp, 0, R->z, M->n, 0, false, R->eps, R->alpha + 1, R->st,
           0, ST_DEGENERATE, R->M->ctx->dprog, 1));
-  int i0 = 1;
-  TRY(run_rows(R, &i0));  // row-streamed persistent kernel (n <= 6144)
-  if (i0 == 1) TRY(run_stream(R, &i0));  // persistent kernel for the steps whose tiles fit
-  if (i0 > R->k_max) return read_state(R);
-  return run_steps(R, i0);
+  return run_steps(R, 1);
 }
 
 // GK steps i0..k_max (step i: A p_i and A^T q_{i+1} with their CGS2)
 static int run_steps(ksvd_run* R, int i0) {
   ksvd_mat* M = R->M;
   ksvd_ctx* c = M->ctx;
-  // Pacing: the host enqueues step i only once step i-kLag has finished.
-  // KSVD_PACE=spin polls the mapped progress word; the default waits on a
-  // ring of events (which also flushes the launch queue).  Either way the
+  // Pacing: the host enqueues step i only once step i-kLag has finished,
+  // waiting on a ring of events (which also flushes the launch queue).  The
   // stop decision is "the run halted at a step <= i-kLag", which depends only
   // on values identical on every rank, so all ranks enqueue the same steps.
-  static const bool spin_mode = [] {
-    const char* e = getenv("KSVD_PACE");
-    return e && strcmp(e, "spin") == 0;
-  }();
+  // (Polling a per-step progress word in mapped memory instead measured no
+  // faster: its system-scope release store sat on the step's critical path.)
   static const bool dbg = getenv("KSVD_DEBUG_HOST") != nullptr;
   using clk = std::chrono::steady_clock;
   double t_launch = 0, t_wait = 0;
@@ -1555,33 +1184,13 @@ static int run_steps(ksvd_run* R, int i0) {
     auto t0 = clk::now();
     if (i - i0 >= kLag) {
       const int s = i - kLag;
-      if (spin_mode) {
-        for (int spin = 0;; ++spin) {
-          const int prog = *(volatile int*)&c->hprog->prog;
-          std::atomic_thread_fence(std::memory_order_acquire);
-          if (*(volatile int*)&c->hprog->halt_step <= s || prog >= 2 * s + 1) break;
-          if ((spin & 1023) == 1023) {
-            const cudaError_t q = cudaStreamQuery(c->stream);
-            if (q != cudaSuccess && q != cudaErrorNotReady)
-              return set_err(KSVD_ERUNTIME, "GK loop: %s", cudaGetErrorString(q));
-          }
-          _mm_pause();
-        }
-      } else {
-        CK(cudaEventSynchronize(c->ring_ev[s % kRing]));
-      }
+      CK(cudaEventSynchronize(c->ring_ev[s % kRing]));
       std::atomic_thread_fence(std::memory_order_acquire);
       if (*(volatile int*)&c->hprog->halt_step <= s) break;
     }
     auto t1 = clk::now();
     TRY(enqueue_step(R, i));
-    if (spin_mode) {
-      const cudaError_t q = cudaStreamQuery(c->stream);  // flush the launch queue
-      if (q != cudaSuccess && q != cudaErrorNotReady)
-        return set_err(KSVD_ERUNTIME, "GK loop: %s", cudaGetErrorString(q));
-    } else {
-      CK(cudaEventRecord(c->ring_ev[i % kRing], c->stream));
-    }
+    CK(cudaEventRecord(c->ring_ev[i % kRing], c->stream));
     auto t2 = clk::now();
     t_wait += std::chrono::duration<double, std::milli>(t1 - t0).count();
     t_launch += std::chrono::duration<double, std::milli>(t2 - t1).count();
@@ -1602,7 +1211,6 @@ static int run_steps(ksvd_run* R, int i0) {
             "rest %.1f), wait %.3f ms, launches %lld\n", R->k_max, t_launch, g_tsec[0],
             g_tsec[1], g_tsec[5] - g_tsec[1], t_wait, (long long)c->launches);
   for (double& v : g_tsec) v = 0;
-  TRY(set_l2_window(M, false));
   return read_state(R);
 }
 
@@ -1625,12 +1233,7 @@ static int enqueue_multi_rhs(ksvd_mat* M, const double* X, int64_t ldx, int k,
   if (cdiv(M->mloc, kMR) * cdiv(k, kMC) < M->ctx->sms && xs_bytes <= kResidentSmemMax) {
     // too few 256-row tiles to fill the GPU: one CTA per SM, X in shared
     // memory, one warp per row
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(k_multi_rhs_rows<TA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)kResidentSmemMax));
-      attr = true;
-    }
+    TRY(smem_attr((const void*)k_multi_rhs_rows<TA>, M->ctx->device, (int)kResidentSmemMax));
     const int64_t G = std::min<int64_t>(M->ctx->sms, cdiv(M->mloc, kWarps));
     const int rpc = (int)cdiv(M->mloc, G);
     for (int t0 = 0; t0 < k; t0 += 32) {
@@ -1642,12 +1245,7 @@ static int enqueue_multi_rhs(ksvd_mat* M, const double* X, int64_t ldx, int k,
     }
     return 0;
   }
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_multi_rhs<TA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)multi_rhs_smem<TA>()));
-    attr = true;
-  }
+  TRY(smem_attr((const void*)k_multi_rhs<TA>, M->ctx->device, (int)multi_rhs_smem<TA>()));
   dim3 grid((unsigned)cdiv(M->mloc, kMR), (unsigned)cdiv(k, kMC));
   return launch(M->ctx, KC_OTHER, k_multi_rhs<TA>, grid, dim3(kThreads), multi_rhs_smem<TA>(),
                 (const TA*)M->A, M->lda, M->mloc, M->n, X, ldx, k, sigma, Y, ldy);
@@ -1999,14 +1597,8 @@ static bool resident_plan(ksvd_run* Rn, ResidentPlan* pl) {
 }
 
 template <typename TA>
-static int resident_attr() {
-  static bool done = false;
-  if (!done) {
-    CK(cudaFuncSetAttribute(k_gk_resident<TA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)kResidentSmemMax));
-    done = true;
-  }
-  return 0;
+static int resident_attr(int device) {
+  return smem_attr((const void*)k_gk_resident<TA>, device, (int)kResidentSmemMax);
 }
 
 // q1_local: the start vector (fresh run, l = 0), or nullptr to resume after
@@ -2050,10 +1642,10 @@ static int run_resident(ksvd_run* Rn, const ResidentPlan& pl, const double* q1_l
   void* args[] = {&a};
   const void* kern;
   if (M->dtype == KSVD_F32) {
-    TRY(resident_attr<float>());
+    TRY(resident_attr<float>(c->device));
     kern = (const void*)k_gk_resident<float>;
   } else {
-    TRY(resident_attr<double>());
+    TRY(resident_attr<double>(c->device));
     kern = (const void*)k_gk_resident<double>;
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -2104,6 +1696,32 @@ int ksvd_nccl_unique_id(char* uid) {
   return 0;
 }
 
+// Do all c->sms CTAs of a one-CTA-per-SM kernel become resident at once?
+// The grid-synchronised kernels (k_cgs2_tile2, k_cgs_tile_phase) rely on it
+// for their regular launches; an SM-limited MPS client or green context
+// breaks it, and the context then launches them cooperatively (the driver
+// checks residency and fails the launch cleanly instead).  KSVD_FORCE_COOP=1
+// forces the cooperative launches (tests).
+static int residency_probe(ksvd_ctx* c) {
+  if (getenv("KSVD_FORCE_COOP")) {
+    c->coop_cgs = true;
+    return 0;
+  }
+  TRY(smem_attr((const void*)k_residency_probe, c->device, (int)kTileSmemMax));
+  unsigned* cnt = nullptr;
+  CK(cudaMalloc(&cnt, 16));
+  CK(cudaMemsetAsync(cnt, 0, 16, c->stream));
+  k_residency_probe<<<c->sms, kThreads, kTileSmemMax, c->stream>>>(
+      cnt, reinterpret_cast<int*>(cnt + 2), (unsigned)c->sms);
+  CK(cudaGetLastError());
+  int failed = 0;
+  CK(cudaMemcpyAsync(&failed, cnt + 2, sizeof failed, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaFree(cnt));
+  c->coop_cgs = failed != 0;
+  return 0;
+}
+
 int ksvd_ctx_create(int device, int rank, int nranks, const char* uid, ksvd_ctx** out) {
   if (nranks < 1 || rank < 0 || rank >= nranks)
     return set_err(KSVD_ECONFIG, "bad rank %d / nranks %d", rank, nranks);
@@ -2117,14 +1735,7 @@ int ksvd_ctx_create(int device, int rank, int nranks, const char* uid, ksvd_ctx*
   CK(cudaGetDeviceProperties(&prop, device));
   c->sms = prop.multiProcessorCount;
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-  if (const char* e = getenv("KSVD_PDL_TRIG")) {
-    const int trig = atoi(e);
-    CK(cudaMemcpyToSymbol(g_pdl_trig, &trig, sizeof trig));
-  }
-  if (const char* e = getenv("KSVD_PACE")) {  // run_steps: progress-word pacing
-    const int spin = strcmp(e, "spin") == 0 ? 1 : 0;
-    CK(cudaMemcpyToSymbol(g_spin_pace, &spin, sizeof spin));
-  }
+  TRY(residency_probe(c));
   for (auto& e : c->marks) CK(cudaEventCreate(&e));
   for (auto& e : c->ring_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaHostAlloc((void**)&c->hprog, sizeof(HostProg), cudaHostAllocMapped));
@@ -2705,12 +2316,7 @@ int ksvd_dense_svd_dev(ksvd_ctx* c, int k, const double* T, double* U, double* s
   const size_t smem = sizeof(double) * (2 * (size_t)kk * k + kk);
   if (smem > kResidentSmemMax) return ksvd_dense_svd(k, T, U, s, V);  // host Jacobi
   CK(cudaSetDevice(c->device));
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_dense_svd_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)kResidentSmemMax));
-    attr = true;
-  }
+  TRY(smem_attr((const void*)k_dense_svd_cta, c->device, (int)kResidentSmemMax));
   cudaStream_t st = c->stream;
   const size_t kk2 = (size_t)k * k;
   double* buf = nullptr;
@@ -2866,8 +2472,10 @@ int ksvd_run_info(ksvd_run* R, int* k_prime, int* flags, double* alphas, double*
   if (k_prime) *k_prime = R->kprime;
   if (flags) *flags = R->flags;
   const int kp = R->kprime;
-  if (alphas && kp > 0)
-    CK(cudaMemcpyAsync(alphas, R->alpha + 1, sizeof(double) * kp, cudaMemcpyDeviceToHost,
+  // + alpha_{k'+1} after an alpha breakdown (its residual, see the header)
+  const int na = kp + ((R->flags & KSVD_RUN_ALPHA_BREAK) && kp < R->k_max ? 1 : 0);
+  if (alphas && na > 0)
+    CK(cudaMemcpyAsync(alphas, R->alpha + 1, sizeof(double) * na, cudaMemcpyDeviceToHost,
                        c->stream));
   // betas[1..k'] = beta_2..beta_{k'+1}
   if (betas && kp > 0 && !(R->flags & KSVD_RUN_DEGENERATE))
@@ -2960,12 +2568,7 @@ int ksvd_ritz(ksvd_run* R, const double* G, const double* sigma, int take, int o
   if (ortho && c->comm == nullptr && uf_smem <= kResidentSmemMax) {
     // the same filter in one single-CTA launch (U fits shared memory)
     TRY(reset_state(c, R->st_aux));
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(k_ufilter_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)kResidentSmemMax));
-      attr = true;
-    }
+    TRY(smem_attr((const void*)k_ufilter_small, c->device, (int)kResidentSmemMax));
     TRY(launch(c, KC_OTHER, k_ufilter_small, dim3(1), dim3(kUfThreads), uf_smem, R->U, ldu,
                (int)M->mloc, take, ldm, 1e-2, R->st_aux));
     DevState h{};
@@ -3072,7 +2675,6 @@ int ksvd_run_restart(ksvd_run* R, int l, const double* X, const double* Y, int k
   c->hprog->status = 0;
   ResidentPlan pl;
   if (resident_plan(R, &pl)) return run_resident(R, pl, nullptr, l);
-  TRY(set_l2_window(M, true));
   // z = A^T q_{l+1}; CGS2 against the l kept right Ritz vectors (the spike);
   // alpha_{l+1} < eps: the kept space is invariant (k' = l)
   TRY(enqueue_gemv_t(M, R->Q + (size_t)l * R->ldq, nullptr, nullptr, nullptr, nullptr, R->z,

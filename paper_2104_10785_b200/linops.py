@@ -296,22 +296,29 @@ def as_operator(A) -> DeviceMatrix:
             if A.dim() != 2:
                 raise ShapeMismatchError(f"expected a 2-d matrix, got shape {tuple(A.shape)}")
             ctx = _lib.get_context()
-            t = A
+            m = int(A.shape[0])
+            r0, ml = row_partition(m, ctx.nranks, ctx.rank)
+            # this rank's rows first: a large A on one GPU is never copied
+            # whole to every rank's device, nor up-cast whole
+            t = A[r0:r0 + ml]
             if t.device.index != ctx.device:
                 t = t.to(f"cuda:{ctx.device}")
             if t.dtype not in (torch.float64, torch.float32):
                 t = t.to(torch.float64)
-            m = int(t.shape[0])
-            r0, ml = row_partition(m, ctx.nranks, ctx.rank)
-            t = t[r0:r0 + ml]
             if t.dim() != 2 or (ml > 0 and t.stride(1) != 1) or (ml > 1 and t.stride(0) < t.shape[1]):
                 t = t.contiguous()
             return DeviceMatrix.from_torch(t, ctx=ctx, row0=r0, m_global=m)
     except ImportError:
         pass
     A = np.asarray(A)
+    if A.ndim != 2:
+        raise ShapeMismatchError(f"expected a 2-d matrix, got shape {A.shape}")
     if A.dtype not in (np.float32, np.float64):
-        A = A.astype(np.float64)
+        # up-cast only this rank's rows (the reference coerces to f64, linops.py:82-86)
+        ctx = _lib.get_context()
+        r0, ml = row_partition(int(A.shape[0]), ctx.nranks, ctx.rank)
+        return DeviceMatrix.from_host(np.asarray(A[r0:r0 + ml], dtype=np.float64), ctx=ctx,
+                                      rows_are_local=True, m_global=int(A.shape[0]), row0=r0)
     return DeviceMatrix.from_host(A)
 
 

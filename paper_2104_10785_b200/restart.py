@@ -135,12 +135,20 @@ def fsvd_restarted(A, r: int, k: int | None = None, tol: float = 1e-10,
             T, kq, kpc = _projected(a, b, kp, flags, head)
             Uh, s, Vh = dense_svd(T)  # host Jacobi: faster than the 1-CTA kernel at k <= 100
             early = bool(flags & _lib.RUN_EARLY)
-            resid = np.zeros(T.shape[0]) if early else abs(b[kp]) * np.abs(Uh[kp - 1, :])
+            if flags & _lib.RUN_ALPHA_BREAK:
+                # A v_i = s_i u_i exactly; the residual sits on the other
+                # side: A^T u_i - s_i v_i = alpha_{k'+1} Vh[k', i] p_{k'+1}
+                resid = abs(a[kp]) * np.abs(Vh[kp, :])
+            else:
+                # rho_i = beta_{k'+1} Uh[k'-1, i] (beta_{k'+1} < eps on a beta
+                # breakdown: small, not zero)
+                resid = abs(b[kp]) * np.abs(Uh[kp - 1, :])
             s1 = float(s[0]) if s.size else 0.0
             n_keep = int((s > DROP_REL * s1).sum())
             take = min(r, n_keep)
-            converged = early or bool(np.all(resid[:take] <= tol * s1))
-            if converged or restarts >= max_restarts or k >= kmax:
+            converged = bool(np.all(resid[:take] <= tol * s1))
+            # a breakdown exhausted the Krylov space: nothing to restart from
+            if converged or early or restarts >= max_restarts or k >= kmax:
                 break
             l = l_keep
             X = _colmajor(Vh[:, :l])

@@ -280,28 +280,24 @@ print(json.dumps(out))
 _MULTI = {"KSVD_RESIDENT": "0"}  # small cases would otherwise take the resident kernel
 
 
-@pytest.mark.parametrize("env", [{"KSVD_TILE": "0", **_MULTI}, {"KSVD_COOP": "0", **_MULTI},
+@pytest.mark.parametrize("env", [{"KSVD_COOP": "0", **_MULTI},
                                  {"KSVD_FORCE_NCCL": "1"}, {"KSVD_FORCE_PX": "1"},
                                  {"KSVD_FORCE_NCCL": "1", "KSVD_MTILE": "0"},
                                  {"KSVD_FORCE_PX": "1", "KSVD_MTILE": "0"},
                                  {"KSVD_FORCE_NCCL": "1", "KSVD_PDL_MULTI": "0"},
-                                 {"KSVD_COOP_GLOBAL": "1", "KSVD_TILE": "0", **_MULTI},
-                                 {"KSVD_CGS_SYNC": "5", **_MULTI}, {"KSVD_RED_MAX": "0", **_MULTI},
+                                 {"KSVD_FORCE_NCCL": "1", "KSVD_FORCE_COOP": "1"},
+                                 {"KSVD_RED_MAX": "0", **_MULTI},
                                  {"KSVD_RED_MAX": "100000000", **_MULTI}, {"KSVD_PDL": "0", **_MULTI},
-                                 {"KSVD_PDL_TRIG": "3", **_MULTI}, {"KSVD_STREAM": "1", **_MULTI},
-                                 {"KSVD_ROWS": "1", **_MULTI},
-                                 {"KSVD_COOP_LAUNCH": "1", **_MULTI},
-                                 {"KSVD_FLAG_BARRIER": "1", **_MULTI},
-                                 {"KSVD_PACE": "spin", **_MULTI},
-                                 {"KSVD_COOP_LAUNCH": "1", "KSVD_CGS_SYNC": "5", **_MULTI},
+                                 {"KSVD_FORCE_COOP": "1", **_MULTI},
                                  _MULTI, {}])
 def test_cgs_paths_agree(env):
-    """The whole-loop resident kernel (small matrices, default), the tile-resident (2-round k_cgs2_tile2 with redundant or distributed
-    reductions, 5-round k_cgs2_tile), global-load cooperative and
-    multi-kernel CGS2 paths (selected at load time) all meet the parity bar,
-    with and without programmatic dependent launch, launched regularly with
-    the flip grid barrier (default) or cooperatively; KSVD_FORCE_NCCL runs the
-    multi-rank code path (NCCL all-reduces between the kernels) over a
+    """The whole-loop resident kernel (small matrices, default), the
+    tile-resident k_cgs2_tile2 (redundant or distributed reductions) and the
+    multi-kernel CGS2 path (KSVD_COOP=0) all meet the parity bar, with and
+    without programmatic dependent launch, launched regularly with the flip
+    grid barrier (default) or cooperatively (KSVD_FORCE_COOP: the fallback
+    when the residency probe fails); KSVD_FORCE_NCCL runs the multi-rank code
+    path (NCCL all-reduces between the kernels, k_cgs_tile_phase) over a
     1-rank communicator, KSVD_FORCE_PX the same path with every all-reduce
     through the NVLink peer-exchange kernel (csrc/peer.cuh) instead."""
     import json

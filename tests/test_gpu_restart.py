@@ -130,3 +130,19 @@ def test_dense_svd_single_cta_kernel():
         assert np.allclose((Uh * s) @ Vh.T, T, atol=1e-12 * ref[0]), k
         assert np.allclose(Vh.T @ Vh, np.eye(k), atol=1e-12), k
         assert np.all(np.diff(s) <= 0)
+
+
+def test_breakdown_residual_reported_not_zeroed():
+    """A GK breakdown (beta_{k'+1} < eps, ABSOLUTE 1e-8) is not convergence
+    at a tighter tol: the residuals come from the breakdown scalar and the
+    same tol test decides `converged`.  A = rank 6 + 1e-10 noise:
+    beta_7 ~ 4e-9 < eps breaks the loop at k' = 6, far above tol * s_1."""
+    A = synth.low_rank_synth(500, 300, 6, seed=2)
+    A = A + 1e-10 * np.random.default_rng(5).standard_normal(A.shape)
+    tol = 1e-14
+    ps, info = K.fsvd_restarted(A, 4, k=12, tol=tol, cfg=K.BidiagConfig(k_max=12, seed=3))
+    true_res = np.linalg.norm(A @ ps.V - ps.U * ps.sigma, axis=0)
+    assert np.all(info.residuals > 0)
+    assert info.converged == bool(np.all(info.residuals <= tol * ps.sigma[0]))
+    assert not info.converged
+    np.testing.assert_allclose(true_res, info.residuals, rtol=0.05, atol=1e-13 * ps.sigma[0])
