@@ -132,7 +132,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
 // sum_{k < cnt} p[k*ld] with up to 16 loads in flight (predicated, so a
 // whole batch is one L2 round trip) and 4 interleaved partial sums combined
 // in a fixed order (deterministic; not latency-chained).  The finalisation
-// of k_gemv_n2's 20 chunk partials (config 2) is 2 round trips, not 3.
+// of k_gemv_n's chunk-group partials is one or two round trips.
 __device__ __forceinline__ double strided_sum(const double* __restrict__ p, int64_t ld,
                                               int cnt) {
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
@@ -179,55 +179,59 @@ __device__ __forceinline__ void flag_nonfinite(DevState* st, double v, int step)
 }
 
 // ---------------------------------------------------------------------------
-// gemv_n, column-chunked (k_gemv_n2): w = A p   (bidiag.py:152)
-//
-// Each warp owns one column chunk of 32*U 16-byte vectors and a range of
-// rows.  Its slice of p (p = p_src / *p_scale, the deferred normalisation
-// of P[:, i-1]) is loaded once into registers; the warp then streams 8 rows
-// per iteration (8*U independent 16-byte loads per lane in flight), forms
-// the 8 row partials, and reduces them across the warp with one 9-shuffle
-// transpose butterfly (warp_sum8).  Warps of a CTA take consecutive chunks
-// of the same rows, so a CTA reads long contiguous row segments.  Partials
-// per (chunk, row) go to part[chunk*m + row]; k_gemv_n_finalize adds them
-// in chunk order and applies - alpha q.
-// Loads of vectors another CTA wrote: through L2 (ld.global.cg) inside a
-// persistent kernel (L1 is not coherent), plain cached loads otherwise --
-// measured: the L1 reuse of p / q across a standalone launch's CTAs is worth
-// 1-4 % of the A-streaming kernels.
 template <bool CG>
 __device__ __forceinline__ double ldv(const double* p) {
   if constexpr (CG) return __ldcg(p);
   else return *p;
 }
 
-// The body is a device function; CG = true sends p, its scale and the
-// partials through L2 (__ldcg), for callers whose other CTAs wrote them in
-// the same launch.
-template <typename TA, int U, int RB = 8, int PF = 0, bool CG = false>
-__device__ __forceinline__ void gemv_n2_body(const TA* __restrict__ A, int64_t lda, int64_t m,
-                                             int64_t nvec, int nchunks, int64_t nseg,
-                                             const double* __restrict__ p_src,
-                                             const double* __restrict__ p_scale,
-                                             double* __restrict__ p_dst, int64_t n_true,
-                                             double* __restrict__ part, int64_t gw) {
-  static_assert(RB % 8 == 0, "rows per iteration: multiple of 8");
+// gemv_n (k_gemv_n): w = A p   (bidiag.py:152)
+//
+// Each warp owns one column chunk of 32*U 16-byte vectors; its slice of p
+// (p = p_src / *p_scale, the deferred normalisation of P[:, i-1], written
+// back to p_dst by the first row segment) is loaded once into registers.
+// The 8 warps of a CTA take 8 consecutive chunks of the SAME rows: a CTA
+// streams 8 rows x 8 chunks per iteration (8*U independent 16-byte loads per
+// lane in flight), each warp reduces its 8 row partials across the warp with
+// one 9-shuffle transpose butterfly (warp_sum8), and the 8 warps' partials
+// are summed in shared memory in warp order and written once per (chunk
+// group, row).  Measured on B200 (tools/gemv_bench.cu): 7.11 TB/s on a 40 GB
+// f32 matrix and 7.31 TB/s on 32 GB f64, against 6.65 / 6.87 for the same
+// loads with one partial store per warp and no CTA-level sum (the earlier
+// k_gemv_n2) -- at the rate of the column-reduction kernel k_gemv_t2.
+// CTA b: chunk group b % ngroups, row segment b / ngroups of nseg (rows
+// rseg*8 + k*nseg*8: all CTAs move down the matrix as one band, so the rows
+// read last stay in L2 for k_gemv_t2, which sweeps up).  Partials go to
+// part[group * m + row]; k_gemv_n_finalize (or the CGS2 kernels' fused
+// finalisation) adds them in group order and applies - alpha q.
+template <typename TA, int U>
+__global__ void __launch_bounds__(kThreads)
+k_gemv_n(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nchunks,
+          int ngroups, int64_t nseg, const double* __restrict__ p_src,
+          const double* __restrict__ p_scale, double* __restrict__ p_dst, int64_t n_true,
+          double* __restrict__ part, const DevState* st) {
+  pdl_wait();
+  pdl_trigger(1);
+  if (halted(st)) return;
   constexpr int V = AVec<TA>::V;
   constexpr int CW = 32 * U;
-  const int lane = threadIdx.x & 31;
-  const int chunk = (int)(gw % nchunks);
-  const int64_t rseg = gw / nchunks;
+  __shared__ double red[2][kWarps][8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = (int)(blockIdx.x % ngroups);
+  const int64_t rseg = blockIdx.x / ngroups;
   if (rseg >= nseg) return;
-  const double scale = p_scale ? ldv<CG>(p_scale) : 1.0;
+  const int chunk = grp * kWarps + warp;
+  const double scale = p_scale ? *p_scale : 1.0;
   double pv[U][V];
   bool live[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const int64_t vi = (int64_t)chunk * CW + u * 32 + lane;
-    live[u] = vi < nvec;
+    live[u] = chunk < nchunks && vi < nvec;
 #pragma unroll
     for (int k = 0; k < V; ++k) {
       const int64_t col = vi * V + k;
-      double x = (live[u] && col < n_true) ? ldv<CG>(p_src + col) : 0.0;
+      double x = (live[u] && col < n_true) ? p_src[col] : 0.0;
       if (p_scale) {
         x = x / scale;
         if (rseg == 0 && p_dst && live[u] && col < n_true) p_dst[col] = x;
@@ -236,63 +240,39 @@ __device__ __forceinline__ void gemv_n2_body(const TA* __restrict__ A, int64_t l
     }
   }
   const TA* base = A + ((int64_t)chunk * CW + lane) * V;
-  // row blocks rseg, rseg + nseg, ...: all warps move down the matrix as one
-  // band, so the rows read last stay in L2 for k_gemv_t, which sweeps up.
-  // Lanes 0..RB-1 also issue bulk L2 prefetches (cp.async.bulk.prefetch) of
-  // this warp's chunk of the rows PF iterations ahead: memory-level
-  // parallelism without holding registers for it.
-  const int64_t pf_vecs = nvec - (int64_t)chunk * CW < CW ? nvec - (int64_t)chunk * CW : (int64_t)CW;
-  const uint32_t pf_bytes = (uint32_t)(pf_vecs * 16);
-  const TA* pf_base = A + (int64_t)chunk * CW * V;
-  for (int64_t r = rseg * RB; r < m; r += nseg * RB) {
-    const int64_t r_end = min(m, r + RB);
-    if (PF > 0 && lane < RB) {
-      const int64_t rp = r + (int64_t)PF * nseg * RB + lane;
-      if (rp < m)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf_base + rp * lda),
-                     "r"(pf_bytes)
-                     : "memory");
-    }
-    AVec<TA> a[RB][U];
+  int par = 0;
+  for (int64_t r = rseg * 8; r < m; r += nseg * 8, par ^= 1) {
+    AVec<TA> a[8][U];
 #pragma unroll
-    for (int rr = 0; rr < RB; ++rr) {
-      const int64_t row = min(r + rr, r_end - 1);  // clamp: duplicate rows are discarded
+    for (int rr = 0; rr < 8; ++rr) {
+      const int64_t row = min(r + rr, m - 1);  // clamp: duplicate rows are discarded
 #pragma unroll
       for (int u = 0; u < U; ++u)
         if (live[u]) a[rr][u].load(base + row * lda + u * 32 * V);
     }
+    double v[8];
 #pragma unroll
-    for (int h = 0; h < RB / 8; ++h) {
-      double v[8];
+    for (int rr = 0; rr < 8; ++rr) {
+      double s = 0.0;
 #pragma unroll
-      for (int rr = 0; rr < 8; ++rr) {
-        double s = 0.0;
+      for (int u = 0; u < U; ++u)
+        if (live[u]) {
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (live[u]) {
+          for (int k = 0; k < V; ++k) s = fma(a[rr][u].get(k), pv[u][k], s);
+        }
+      v[rr] = s;
+    }
+    const double t = warp_sum8(v);
+    if ((lane & 3) == 0) red[par][warp][warp_sum8_index(lane)] = t;
+    __syncthreads();  // red[par] complete; red[par ^ 1] free again (read last round)
+    if (warp == 0 && lane < 8) {
+      double sum = red[par][0][lane];
 #pragma unroll
-            for (int k = 0; k < V; ++k) s = fma(a[h * 8 + rr][u].get(k), pv[u][k], s);
-          }
-        v[rr] = s;
-      }
-      const double t = warp_sum8(v);
-      const int64_t row = r + h * 8 + warp_sum8_index(lane);
-      if ((lane & 3) == 0 && row < r_end) part[(int64_t)chunk * m + row] = t;
+      for (int w = 1; w < kWarps; ++w) sum += red[par][w][lane];
+      const int64_t row = r + lane;
+      if (row < m) part[(int64_t)grp * m + row] = sum;
     }
   }
-}
-
-template <typename TA, int U, int RB = 8, int PF = 0>
-__global__ void __launch_bounds__(kThreads)
-k_gemv_n2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nchunks,
-          int64_t nseg, const double* __restrict__ p_src,
-          const double* __restrict__ p_scale, double* __restrict__ p_dst, int64_t n_true,
-          double* __restrict__ part, const DevState* st) {
-  pdl_wait();
-  pdl_trigger(1);
-  if (halted(st)) return;
-  gemv_n2_body<TA, U, RB, PF>(A, lda, m, nvec, nchunks, nseg, p_src, p_scale, p_dst, n_true,
-                              part, (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5));
 }
 
 // w[r] = sum_chunks part[c][r] - alpha q[r]  (chunk order fixed)
@@ -423,7 +403,7 @@ k_gemv_t(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
 // k_gemv_t with the row blocks of its split interleaved across the splits
 // and visited bottom-up (block = RG*U*IT rows; CTA s takes blocks s,
 // s + nsplit, ... from the last one): the whole grid then sweeps A upwards as
-// one band, starting on the rows k_gemv_n2 (top-down band) left in L2.
+// one band, starting on the rows k_gemv_n (top-down band) left in L2.
 // Shared-memory needs of gemv_t2_body (q staging + group sums), so callers
 // can provide them (static in k_gemv_t2, part of the dynamic carve-out in
 // the persistent kernel).
@@ -1214,7 +1194,7 @@ k_cgs2_tile2(CgsCoopArgs a) {
 // the passes of k_cgs2_tile2 as three launches, the host's all-reduces of
 // the coefficient vector between them (the multi-kernel path needs eight
 // launches for the same CGS2):
-//   phase 0: finalisation of k_gemv_n2's chunk partials (x = A p - alpha q),
+//   phase 0: finalisation of k_gemv_n's chunk-group partials (x = A p - alpha q),
 //            partial B^T x -> grid barrier -> distributed column sums -> c
 //   phase 1: x -= B c (c all-reduced by the host) ; partial B^T x -> ... -> c
 //   phase 2: x -= B c ; ||x||^2 of this rank's rows (CTA 0, fixed order) and

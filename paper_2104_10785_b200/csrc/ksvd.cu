@@ -166,7 +166,7 @@ static int collect_profile(ksvd_ctx* c) {
 // griddepcontrol.wait.  Every kernel launched this way calls pdl_wait() in
 // every CTA before touching its predecessor's outputs (kernels.cuh).
 // Multi-rank: only our own step kernels carry the attribute; the kernels
-// that trigger early (k_gemv_n2, k_gemv_t2) are always followed by one of
+// that trigger early (k_gemv_n, k_gemv_t2) are always followed by one of
 // ours, never directly by a collective, so an NCCL kernel never starts
 // before its input is complete (KSVD_PDL_MULTI=0 disables PDL there).
 static bool pdl_enabled(const ksvd_ctx* c) {
@@ -269,17 +269,15 @@ static int allreduce(ksvd_ctx* c, double* buf, size_t count) {
 // ---------------------------------------------------------------------------
 // matrices
 struct GemvNPlan {
-  int V, U, nchunks;
-  int pf = 0;  // k_gemv_n2 PF: bulk L2 prefetch one row block ahead (large A)
-  int64_t nvec, rows_per_warp, blocks;
+  int V, U, nchunks, ngroups;  // ngroups: partial sums per row (chunk groups of 8)
+  int64_t nvec, nseg, blocks;
 };
 struct GemvTPlan {
   int64_t ncoltiles, nsplit, rows_per_split;
   int rg;  // row groups per CTA (k_gemv_t RG)
 };
 
-constexpr int kUnrollN64 = 4;  // U of k_gemv_n2 for f64 A (32*U 16-byte vectors / chunk)
-constexpr int kUnrollN32 = 2;  // U of k_gemv_n2 for f32 A
+constexpr int kUnrollN = 2;  // U of k_gemv_n (32*U 16-byte vectors per warp chunk)
 constexpr int kUnrollT = 16;   // U of k_gemv_t
 constexpr int kGemvTCtasPerSm = 4;
 
@@ -291,7 +289,7 @@ struct ksvd_mat {
   void* A = nullptr;
   GemvNPlan pn{};
   GemvTPlan pt{};
-  double* part_n = nullptr;  // nchunks x mloc  (nchunks > 1)
+  double* part_n = nullptr;  // ngroups x mloc: k_gemv_n partial row sums
   double* part_t = nullptr;  // nsplit x n_pad
   // plain-product scratch
   double *dx = nullptr, *dy = nullptr;
@@ -311,9 +309,9 @@ struct ksvd_mat {
 
 static size_t esize(int dtype) { return dtype == KSVD_F32 ? 4 : 8; }
 
-template <typename TA, int U>
-static int occupancy_n2(int* out) {
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k_gemv_n2<TA, U>, kThreads, 0));
+template <typename TA>
+static int occupancy_n(int* out) {
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k_gemv_n<TA, kUnrollN>, kThreads, 0));
   return 0;
 }
 
@@ -322,31 +320,21 @@ static int plan_matrix(ksvd_mat* M) {
   const int64_t bytes = esize(M->dtype);
   GemvNPlan& pn = M->pn;
   pn.V = (int)(16 / bytes);
-  // KSVD_GEMVN_PF=1: U = 4 with the one-block bulk L2 prefetch.  At full
-  // clocks (tools/gemv_bench.cu) it lifts f32 40 GB from 6.62 to 6.85 TB/s
-  // and f64 32 GB from 6.86 to 6.96, but in the long runs of configs 3-4,
-  // under sw_power_cap at ~1.48 GHz, it measured 3-4 % SLOWER (config 4
-  // gemv_n 6.22 vs 6.50 TB/s, config 3 6.72 vs 6.91; tools/pf_ab.sh), so it
-  // is off by default.
-  pn.pf = 0;
-  if (const char* e = getenv("KSVD_GEMVN_PF")) pn.pf = atoi(e) ? 1 : 0;
-  pn.U = M->dtype == KSVD_F32 ? (pn.pf ? 4 : kUnrollN32) : kUnrollN64;
+  pn.U = kUnrollN;
   pn.nvec = cdiv(M->n, pn.V);
   pn.nchunks = (int)cdiv(pn.nvec, 32 * pn.U);
+  pn.ngroups = (int)cdiv(pn.nchunks, kWarps);
   int occ = 1;
-  if (M->dtype == KSVD_F32 && pn.U == 4)
-    TRY((occupancy_n2<float, 4>(&occ)));
-  else if (M->dtype == KSVD_F32)
-    TRY((occupancy_n2<float, kUnrollN32>(&occ)));
+  if (M->dtype == KSVD_F32)
+    TRY(occupancy_n<float>(&occ));
   else
-    TRY((occupancy_n2<double, kUnrollN64>(&occ)));
+    TRY(occupancy_n<double>(&occ));
   occ = std::max(occ, 1);
-  const int64_t warps = (int64_t)c->sms * occ * kWarps;
-  // warps per chunk (row-block interleave): capped by the 8-row blocks
-  const int64_t rsegs = std::max<int64_t>(
-      1, std::min<int64_t>(warps / pn.nchunks, cdiv(std::max<int64_t>(M->mloc, 1), 8)));
-  pn.rows_per_warp = rsegs;  // = nseg of k_gemv_n2
-  pn.blocks = cdiv(rsegs * pn.nchunks, kWarps);
+  // row segments: one wave of CTAs (ngroups per segment), capped by the
+  // 8-row blocks
+  pn.nseg = std::max<int64_t>(1, std::min<int64_t>((int64_t)c->sms * occ / pn.ngroups,
+                                                   cdiv(std::max<int64_t>(M->mloc, 1), 8)));
+  pn.blocks = pn.nseg * pn.ngroups;
 
   GemvTPlan& pt = M->pt;
   // RG row groups: narrower column tiles -> fewer row splits -> a short
@@ -385,7 +373,7 @@ static int alloc_matrix_buffers(ksvd_mat* M) {
   TRY(plan_matrix(M));
   const size_t vec = sizeof(double) * std::max(M->n_pad, M->m_pad);
   CK(cudaMallocAsync((void**)&M->part_n,
-                     sizeof(double) * M->pn.nchunks * std::max<int64_t>(M->mloc, 1), s));
+                     sizeof(double) * M->pn.ngroups * std::max<int64_t>(M->mloc, 1), s));
   CK(cudaMallocAsync((void**)&M->part_t, sizeof(double) * M->pt.nsplit * M->n_pad, s));
   CK(cudaMallocAsync((void**)&M->dx, vec, s));
   CK(cudaMallocAsync((void**)&M->dy, vec, s));
@@ -417,9 +405,8 @@ static int free_matrix(ksvd_mat* M) {
   return 0;
 }
 
-// w = A p (- alpha q): p_src/p_scale/p_dst per k_gemv_n; out = w (m rows)
-// w = A p (- alpha q): partial row sums per column chunk (k_gemv_n2), then
-// the chunk sums + epilogue (k_gemv_n_finalize) unless the caller fuses the
+// w = A p (- alpha q): partial row sums per chunk group (k_gemv_n), then
+// the group sums + epilogue (k_gemv_n_finalize) unless the caller fuses the
 // finalisation into its k_cgs2_* launch (finalize = false).
 static int dense_gemv_n(ksvd_mat* M, const double* p_src, const double* p_scale,
                         double* p_dst, const double* qprev, const double* alpha,
@@ -428,27 +415,17 @@ static int dense_gemv_n(ksvd_mat* M, const double* p_src, const double* p_scale,
   const GemvNPlan& pn = M->pn;
   if (M->mloc == 0) return 0;
   const dim3 grid((unsigned)pn.blocks);
-#define KSVD_GEMVN(TA, U, PF)                                                              \
-  TRY(launch_step(c, KC_GEMV_N, k_gemv_n2<TA, U, 8, PF>, grid, dim3(kThreads), 0,          \
-                  (const TA*)M->A, M->lda, M->mloc, pn.nvec, pn.nchunks, pn.rows_per_warp, \
-                  p_src, p_scale, p_dst, M->n, M->part_n, (const DevState*)st))
-  if (M->dtype == KSVD_F32) {
-    if (pn.U == 4)
-      KSVD_GEMVN(float, 4, 1);
-    else if (pn.pf)
-      KSVD_GEMVN(float, kUnrollN32, 1);
-    else
-      KSVD_GEMVN(float, kUnrollN32, 0);
-  } else {
-    if (pn.pf)
-      KSVD_GEMVN(double, kUnrollN64, 1);
-    else
-      KSVD_GEMVN(double, kUnrollN64, 0);
-  }
-#undef KSVD_GEMVN
+  if (M->dtype == KSVD_F32)
+    TRY(launch_step(c, KC_GEMV_N, k_gemv_n<float, kUnrollN>, grid, dim3(kThreads), 0,
+                    (const float*)M->A, M->lda, M->mloc, pn.nvec, pn.nchunks, pn.ngroups,
+                    pn.nseg, p_src, p_scale, p_dst, M->n, M->part_n, (const DevState*)st));
+  else
+    TRY(launch_step(c, KC_GEMV_N, k_gemv_n<double, kUnrollN>, grid, dim3(kThreads), 0,
+                    (const double*)M->A, M->lda, M->mloc, pn.nvec, pn.nchunks, pn.ngroups,
+                    pn.nseg, p_src, p_scale, p_dst, M->n, M->part_n, (const DevState*)st));
   if (finalize)
     TRY(launch(c, KC_FIN, k_gemv_n_finalize, dim3((unsigned)cdiv(M->mloc, kThreads)),
-               dim3(kThreads), 0, (const double*)M->part_n, M->mloc, pn.nchunks, M->mloc,
+               dim3(kThreads), 0, (const double*)M->part_n, M->mloc, pn.ngroups, M->mloc,
                qprev, alpha, w, st, step));
   return 0;
 }
@@ -459,7 +436,7 @@ static int launch_gemv_t(ksvd_mat* M, dim3 grid, const double* q_src, const doub
   ksvd_ctx* c = M->ctx;
   const GemvTPlan& pt = M->pt;
   // band-ordered variant (k_gemv_t2): 256-row blocks when A is within a few
-  // L2 capacities (the band starts on what k_gemv_n2 left in L2), 1024-row
+  // L2 capacities (the band starts on what k_gemv_n left in L2), 1024-row
   // blocks otherwise (same access granularity as contiguous splits)
   const size_t abytes = (size_t)M->mloc * M->lda * esize(M->dtype);
   if (pt.rg == 8) {
@@ -541,7 +518,7 @@ struct FinArgs {  // deferred gemv_t finalisation (phase 0 of k_cgs2_tile2)
 // Factored operator products (reference linops.py:192-202):
 //   A p   = L (C (R^T p))      A^T q = R (C^T (L^T q))
 // built from the dense kernels on the sub-matrices plus an s x s core
-// product; the last stage's partial sums have the k_gemv_n2 layout, so the
+// product; the last stage's partial sums have the k_gemv_n layout, so the
 // CGS kernels fuse their finalisation exactly as for a dense A.  Multi-rank:
 // L^T q is the only sharded reduction (an s-length all-reduce); R and C are
 // replicated, so z is identical on every rank without another collective.
@@ -595,12 +572,12 @@ static int enqueue_gemv_t(ksvd_mat* M, const double* q_src, const double* q_scal
 // where the CGS kernels find the last product's partial sums
 static FinArgs fin_left(ksvd_mat* M, const double* alpha, const double* qprev) {
   ksvd_mat* S = M->fac ? M->fac->L : M;
-  return FinArgs{S->part_n, S->mloc, S->mloc > 0 ? S->pn.nchunks : 0, alpha, qprev};
+  return FinArgs{S->part_n, S->mloc, S->mloc > 0 ? S->pn.ngroups : 0, alpha, qprev};
 }
 static FinArgs fin_right(ksvd_mat* M, const double* beta, const double* pprev) {
   if (M->fac) {
     ksvd_mat* S = M->fac->R;
-    return FinArgs{S->part_n, S->mloc, S->pn.nchunks, beta, pprev};
+    return FinArgs{S->part_n, S->mloc, S->pn.ngroups, beta, pprev};
   }
   return FinArgs{M->part_t, M->n_pad, M->mloc > 0 ? (int)M->pt.nsplit : 0, beta, pprev};
 }

@@ -135,14 +135,16 @@ def test_dense_svd_single_cta_kernel():
 def test_breakdown_residual_reported_not_zeroed():
     """A GK breakdown (beta_{k'+1} < eps, ABSOLUTE 1e-8) is not convergence
     at a tighter tol: the residuals come from the breakdown scalar and the
-    same tol test decides `converged`.  A = rank 6 + 1e-10 noise:
-    beta_7 ~ 4e-9 < eps breaks the loop at k' = 6, far above tol * s_1."""
+    same tol test decides `converged`.  A = rank 6 + 1e-10 noise
+    breaks down after 7 steps; the 7th Ritz triplet sits at the noise level
+    with a residual of the order of beta_8 -- far above tol * s_1."""
     A = synth.low_rank_synth(500, 300, 6, seed=2)
     A = A + 1e-10 * np.random.default_rng(5).standard_normal(A.shape)
     tol = 1e-14
-    ps, info = K.fsvd_restarted(A, 4, k=12, tol=tol, cfg=K.BidiagConfig(k_max=12, seed=3))
+    ps, info = K.fsvd_restarted(A, 7, k=12, tol=tol, cfg=K.BidiagConfig(k_max=12, seed=3))
+    assert info.k_prime < 12 and ps.sigma.shape[0] == 7  # broke down early
     true_res = np.linalg.norm(A @ ps.V - ps.U * ps.sigma, axis=0)
     assert np.all(info.residuals > 0)
     assert info.converged == bool(np.all(info.residuals <= tol * ps.sigma[0]))
-    assert not info.converged
+    assert not info.converged and info.residuals[-1] > tol * ps.sigma[0]
     np.testing.assert_allclose(true_res, info.residuals, rtol=0.05, atol=1e-13 * ps.sigma[0])

@@ -1,7 +1,7 @@
 // Micro-benchmark of the A-streaming kernels (kernels.cuh) on B200:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2104_10785_b200/csrc \
 //        -o tools/gemv_bench tools/gemv_bench.cu
-// Times k_gemv_n / k_gemv_t variants (R rows per warp, U unroll, RG groups)
+// Times k_gemv_n (U unroll) / k_gemv_t2 (U rows in flight, RG groups, IT) variants
 // with CUDA events, best of 10, on an m x n matrix (f64 or f32).
 #include <cstdio>
 #include <cstdlib>
@@ -9,66 +9,36 @@
 #include "kernels.cuh"
 using namespace ksvd;
 
-template <typename TA, int U, int RB = 8, int PF = 0>
-float time_n2(const TA* A, int64_t lda, int64_t m, int64_t n, const double* p, double* part,
+template <typename TA, int U>
+float time_n(const TA* A, int64_t lda, int64_t m, int64_t n, const double* p, double* part,
               DevState* st, int sms, int ctas_per_sm) {
   constexpr int V = 16 / sizeof(TA);
   const int64_t nvec = (n + V - 1) / V;
   const int nchunks = (int)((nvec + 32 * U - 1) / (32 * U));
-  auto k = k_gemv_n2<TA, U, RB, PF>;
+  const int ngroups = (nchunks + 7) / 8;
+  auto k = k_gemv_n<TA, U>;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, 0);
   const int per_sm = occ < ctas_per_sm ? occ : ctas_per_sm;
-  const int64_t warps = (int64_t)sms * per_sm * 8;
-  int64_t rsegs = warps / nchunks;
-  if (rsegs < 1) rsegs = 1;
-  const int64_t rpw = rsegs;  // nseg of the band-interleaved kernel
-  const int64_t blocks = (rsegs * nchunks + 7) / 8;
+  int64_t nseg = (int64_t)sms * per_sm / ngroups;
+  if (nseg < 1) nseg = 1;
+  const int64_t blocks = nseg * ngroups;
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   float best = 1e9;
   for (int r = 0; r < 10; ++r) {
     cudaEventRecord(a);
-    k<<<(unsigned)blocks, 256>>>(A, lda, m, nvec, nchunks, rpw, p, nullptr, nullptr, n, part, st);
+    k<<<(unsigned)blocks, 256>>>(A, lda, m, nvec, nchunks, ngroups, nseg, p, nullptr, nullptr, n,
+                                 part, st);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms;
     cudaEventElapsedTime(&ms, a, b);
     best = ms < best ? ms : best;
   }
-  printf("  gemv_n2 PF=%d U=%d RB=%d occ=%d used=%d chunks=%d rows/warp=%lld: %8.1f us  %7.1f GB/s\n", PF, U, RB, occ,
-         per_sm, nchunks, (long long)rpw, 1e3 * best, m * n * sizeof(TA) / (best * 1e-3) / 1e9);
-  return best;
-}
-
-template <typename TA>
-float time_n3(const TA* A, int64_t lda, int64_t m, int64_t n, const double* p, double* part,
-              DevState* st, int sms) {
-  constexpr int V = 16 / sizeof(TA);
-  const int64_t nvec = (n + V - 1) / V;
-  const int nchunks = (int)((nvec + kN3CW - 1) / kN3CW);
-  const int64_t ngroups = (nchunks + kN3Group - 1) / kN3Group;
-  const int64_t rows8 = (m + kN3Rows - 1) / kN3Rows;
-  const int64_t units = ngroups * rows8;
-  auto k = k_gemv_n3<TA>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kN3Smem);
-  cudaEvent_t a, b;
-  cudaEventCreate(&a);
-  cudaEventCreate(&b);
-  float best = 1e9;
-  for (int r = 0; r < 10; ++r) {
-    cudaEventRecord(a);
-    k<<<sms, kN3Threads, kN3Smem>>>(A, lda, m, nvec, nchunks, rows8, units, p, nullptr, nullptr, n, part, st);
-    cudaEventRecord(b);
-    cudaEventSynchronize(b);
-    float ms;
-    cudaEventElapsedTime(&ms, a, b);
-    best = ms < best ? ms : best;
-  }
-  printf("  gemv_n3 (TMA ring) chunks=%d groups=%lld: %8.1f us  %7.1f GB/s  [%s]\n", nchunks,
-         (long long)ngroups, 1e3 * best, m * n * sizeof(TA) / (best * 1e-3) / 1e9,
-         cudaGetErrorString(cudaGetLastError()));
+  printf("  gemv_n U=%d occ=%d used=%d chunks=%d groups=%d nseg=%lld: %8.1f us  %7.1f GB/s\n", U, occ, per_sm, nchunks, ngroups, (long long)nseg,
+         1e3 * best, m * n * sizeof(TA) / (best * 1e-3) / 1e9);
   return best;
 }
 
@@ -150,25 +120,12 @@ void suite(int64_t m, int64_t n, int sms) {
   DevState* st;
   cudaMalloc(&st, sizeof(DevState));
   cudaMemset(st, 0, sizeof(DevState));
-  time_n2<TA, 4, 8, 0>(A, lda, m, n, p, part, st, sms, 8);
-  time_n2<TA, 4, 8, 1>(A, lda, m, n, p, part, st, sms, 8);
-  time_n2<TA, 4, 8, 2>(A, lda, m, n, p, part, st, sms, 8);
-  time_n2<TA, 4, 8, 4>(A, lda, m, n, p, part, st, sms, 8);
-  time_n2<TA, 4, 16, 0>(A, lda, m, n, p, part, st, sms, 8);
-  time_n2<TA, 2, 8, 0>(A, lda, m, n, p, part, st, sms, 8);
-  time_n2<TA, 2, 16, 0>(A, lda, m, n, p, part, st, sms, 8);
-  time_n2<TA, 2, 8, 2>(A, lda, m, n, p, part, st, sms, 8);
-  timet<TA, 16, 8>(A, lda, m, n, w, part, st, sms, 4);
+  time_n<TA, 2>(A, lda, m, n, p, part, st, sms, 8);
+  time_n<TA, 4>(A, lda, m, n, p, part, st, sms, 8);
+  time_n<TA, 1>(A, lda, m, n, p, part, st, sms, 8);
   timet2<TA, 16, 8, 1>(A, lda, m, n, w, part, st, sms, 4);
   timet2<TA, 16, 8, 2>(A, lda, m, n, w, part, st, sms, 4);
   timet2<TA, 16, 8, 8>(A, lda, m, n, w, part, st, sms, 4);
-  timet2<TA, 16, 8, 2>(A, lda, m, n, w, part, st, sms, 8);
-  timet2<TA, 16, 8, 2>(A, lda, m, n, w, part, st, sms, 3);
-  timet2<TA, 16, 8, 2>(A, lda, m, n, w, part, st, sms, 6);
-  timet2<TA, 16, 4, 2>(A, lda, m, n, w, part, st, sms, 4);
-  timet2<TA, 32, 8, 1>(A, lda, m, n, w, part, st, sms, 4);
-  timet2<TA, 32, 4, 2>(A, lda, m, n, w, part, st, sms, 4);
-  timet2<TA, 8, 8, 4>(A, lda, m, n, w, part, st, sms, 4);
   cudaFree(A);
   cudaFree(p);
   cudaFree(w);
