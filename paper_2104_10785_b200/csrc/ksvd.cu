@@ -1982,7 +1982,9 @@ static int staged_copy(ksvd_ctx* c, void* dev, size_t dpitch, void* host, size_t
                        size_t width, int64_t rows, bool to_device) {
   if (rows <= 0) return 0;
   cudaStream_t s = c->stream;
-  if (host_pinned(host)) {
+  // small transfers (< 4 MB) go direct: the driver's own staging is cheap
+  // there, and the first staged call would allocate the pinned ring
+  if (width * (size_t)rows < ((size_t)4 << 20) || host_pinned(host)) {
     CK(cudaMemcpy2DAsync(to_device ? dev : host, to_device ? dpitch : hpitch,
                          to_device ? host : dev, to_device ? hpitch : dpitch, width,
                          (size_t)rows, to_device ? cudaMemcpyHostToDevice
@@ -2505,11 +2507,11 @@ int ksvd_run_bases(ksvd_run* R, double* Q, int q_cols, double* P, int p_cols) {
     return set_err(KSVD_ECONFIG, "bases: %d/%d columns requested, %d allocated", q_cols,
                    p_cols, R->cap);
   if (Q && q_cols > 0 && M->mloc > 0)
-    CK(cudaMemcpy2DAsync(Q, sizeof(double) * M->mloc, R->Q, sizeof(double) * R->ldq,
-                         sizeof(double) * M->mloc, q_cols, cudaMemcpyDeviceToHost, c->stream));
+    TRY(staged_copy(c, R->Q, sizeof(double) * R->ldq, Q, sizeof(double) * M->mloc,
+                      sizeof(double) * M->mloc, q_cols, false));
   if (P && p_cols > 0)
-    CK(cudaMemcpy2DAsync(P, sizeof(double) * M->n, R->P, sizeof(double) * R->ldp,
-                         sizeof(double) * M->n, p_cols, cudaMemcpyDeviceToHost, c->stream));
+    TRY(staged_copy(c, R->P, sizeof(double) * R->ldp, P, sizeof(double) * M->n,
+                      sizeof(double) * M->n, p_cols, false));
   CK(cudaStreamSynchronize(c->stream));
   return 0;
 }
@@ -2576,10 +2578,10 @@ int ksvd_ritz(ksvd_run* R, const double* G, const double* sigma, int take, int o
                ldu, M->mloc));
   if (good > 0) {
     if (M->mloc > 0)
-      CK(cudaMemcpy2DAsync(U, sizeof(double) * M->mloc, R->U, sizeof(double) * ldu,
-                           sizeof(double) * M->mloc, good, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpy2DAsync(V, sizeof(double) * M->n, R->V, sizeof(double) * ldv,
-                         sizeof(double) * M->n, good, cudaMemcpyDeviceToHost, c->stream));
+      TRY(staged_copy(c, R->U, sizeof(double) * ldu, U, sizeof(double) * M->mloc,
+                      sizeof(double) * M->mloc, good, false));
+    TRY(staged_copy(c, R->V, sizeof(double) * ldv, V, sizeof(double) * M->n,
+                      sizeof(double) * M->n, good, false));
   }
   CK(cudaStreamSynchronize(c->stream));
   *n_good = good;
@@ -2687,10 +2689,10 @@ int ksvd_run_ritz_bases(ksvd_run* R, const double* X, int kq, const double* Y, i
   TRY(launch(c, KC_OTHER, k_fix_signs, dim3(take), dim3(kThreads), 0, R->V, ldv, M->n, R->U,
              ldu, M->mloc));
   if (M->mloc > 0)
-    CK(cudaMemcpy2DAsync(U, sizeof(double) * M->mloc, R->U, sizeof(double) * ldu,
-                         sizeof(double) * M->mloc, take, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpy2DAsync(V, sizeof(double) * M->n, R->V, sizeof(double) * ldv,
-                       sizeof(double) * M->n, take, cudaMemcpyDeviceToHost, s));
+    TRY(staged_copy(c, R->U, sizeof(double) * ldu, U, sizeof(double) * M->mloc,
+                      sizeof(double) * M->mloc, take, false));
+  TRY(staged_copy(c, R->V, sizeof(double) * ldv, V, sizeof(double) * M->n,
+                      sizeof(double) * M->n, take, false));
   CK(cudaStreamSynchronize(s));
   return 0;
 }

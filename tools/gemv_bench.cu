@@ -110,7 +110,7 @@ void suite(int64_t m, int64_t n, int sms) {
          (long long)n, m * n * sizeof(TA) / 1e9);
   TA* A;
   cudaMalloc(&A, sizeof(TA) * m * lda);
-  cudaMemset(A, 0, sizeof(TA) * m * lda);
+  cudaMemset(A, 0x3f, sizeof(TA) * m * lda);  // normal nonzero entries
   double *p, *w, *part;
   cudaMalloc(&p, 8 * lda);
   cudaMemset(p, 0, 8 * lda);
@@ -123,6 +123,7 @@ void suite(int64_t m, int64_t n, int sms) {
   time_n<TA, 2>(A, lda, m, n, p, part, st, sms, 8);
   time_n<TA, 4>(A, lda, m, n, p, part, st, sms, 8);
   time_n<TA, 1>(A, lda, m, n, p, part, st, sms, 8);
+
   timet2<TA, 16, 8, 1>(A, lda, m, n, w, part, st, sms, 4);
   timet2<TA, 16, 8, 2>(A, lda, m, n, w, part, st, sms, 4);
   timet2<TA, 16, 8, 8>(A, lda, m, n, w, part, st, sms, 4);
