@@ -1108,55 +1108,55 @@ __device__ __forceinline__ double tile2_rest(const CgsCoopArgs& a, double* tile,
     }
   };
 
-  if (a.ncols == 0 || a.passes == 0) {
-    dot(partb(0), true);
-    grid_barrier(a, G, bk);
-    reduce_all(partb(0), a.ncols, a.ncols + 1);
-    finish(red[a.ncols]);
-  } else {
-    dot(partb(0), a.passes == 1);
-    phase_mark(a.tdbg, 2, tl);
-    for (int pass = 1; pass <= a.passes; ++pass) {
-      const bool last = pass == a.passes;
-      grid_barrier(a, G, bk);
-      phase_mark(a.tdbg, 3, tl);
-      reduce_all(partb(pass - 1), 0, a.ncols + (last ? 1 : 0));
-      phase_mark(a.tdbg, 4, tl);
-      if (!last) {
-        update(false);
-        dot(partb(pass), pass + 1 == a.passes);
-        phase_mark(a.tdbg, 2, tl);
-        continue;
+  // One grid round per coefficient pass (k = 0 .. P-1), the norm riding on
+  // the last one, plus a direct-norm round when the closed form would
+  // cancel (or for an empty basis).  Every helper has ONE call site: inlined
+  // at several sites the kernel overflowed the instruction cache (ncu on
+  // config 2: 19 % of the warp stalls were no_inst at 7.2k SASS instructions).
+  const int P = a.ncols > 0 ? a.passes : 0;
+  bool norm_only = P == 0;
+  for (int k = 0;; ++k) {
+    const bool with_norm = norm_only || k + 1 == P;
+    if (norm_only) {
+      if (warp == kWarps - 1) {
+        double s = 0.0;
+#pragma unroll
+        for (int e = 0; e < MAXE; ++e) s = fma(xv[e], xv[e], s);
+        s = warp_sum(s);
+        if (lane == 0) partb(k)[(int64_t)a.ncols * G + blockIdx.x] = s;
       }
-      // ||x - B c||^2 = ||x||^2 - ||c||^2 for an orthonormal B.  Exact to
-      // rounding while ||c||^2 <= 1e-6 ||x||^2 (always, after a first pass,
-      // away from breakdown); otherwise (or non-finite) take the direct norm
-      // with one more round.  The test reads identical values in every CTA.
-      // ||c||^2: lane-strided partial sums + a butterfly, the same order in
-      // every warp of every CTA (a serial chain of ncols dependent fmas here
-      // was ~3% of the kernel's stall samples)
-      double cc = 0.0;
+    } else {
+      dot(partb(k), with_norm);
+    }
+    phase_mark(a.tdbg, 2, tl);
+    grid_barrier(a, G, bk);
+    phase_mark(a.tdbg, 3, tl);
+    reduce_all(partb(k), norm_only ? a.ncols : 0, a.ncols + (with_norm ? 1 : 0));
+    phase_mark(a.tdbg, 4, tl);
+    if (norm_only) {
+      finish(red[a.ncols]);
+      break;
+    }
+    const bool last = k + 1 == P;
+    // ||x - B c||^2 = ||x||^2 - ||c||^2 for an orthonormal B.  Exact to
+    // rounding while ||c||^2 <= 1e-6 ||x||^2 (always, after a first pass,
+    // away from breakdown); otherwise (or non-finite) take the direct norm
+    // with one more round.  The test reads identical values in every CTA.
+    // ||c||^2: lane-strided partial sums + a butterfly, the same order in
+    // every warp of every CTA
+    double cc = 0.0, nn = 0.0;
+    if (last) {
       for (int j = lane; j < a.ncols; j += 32) cc = fma(red[j], red[j], cc);
       cc = warp_sum(cc);
-      const double nn = red[a.ncols];
-      const bool closed = cc <= 1e-6 * nn;
-      update(true);
-      phase_mark(a.tdbg, 2, tl);
-      if (closed) {
-        finish(nn - cc);
-      } else {
-        if (warp == kWarps - 1) {
-          double s = 0.0;
-#pragma unroll
-          for (int e = 0; e < MAXE; ++e) s = fma(xv[e], xv[e], s);
-          s = warp_sum(s);
-          if (lane == 0) partb(pass)[(int64_t)a.ncols * G + blockIdx.x] = s;
-        }
-        grid_barrier(a, G, bk);
-        reduce_all(partb(pass), a.ncols, a.ncols + 1);
-        finish(red[a.ncols]);
-      }
+      nn = red[a.ncols];
     }
+    update(last);
+    if (!last) continue;
+    if (cc <= 1e-6 * nn) {
+      finish(nn - cc);
+      break;
+    }
+    norm_only = true;
   }
   if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long now;
