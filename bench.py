@@ -521,21 +521,6 @@ def run_ours(args, rank, world, dist):
             "max_residual_over_sigma1": float(np.max(info.residuals) / ps.sigma[0]),
         }
 
-    # ---- CPU baseline (rank 0, N=1), before the host copy of A exists ----
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        smp = CpuSample(W, A_host, sample_rows=args.sample_rows)
-        v, desc, dt = smp.run()
-        cpu = {"value": v, "unit": UNIT, "cores": blas_threads(), "kind": "port",
-               "sample": desc, "seconds": dt}
-        del smp
-        if converged is not None:
-            from oracle.restarted import restarted_oracle
-
-            t0 = time.perf_counter()
-            restarted_oracle(A_host, 10, 30, tol=1e-10, seed=W["seed"])
-            converged["cpu_port_ms"] = 1e3 * (time.perf_counter() - t0)
-
     # ---- e2e through the public API, from a plain host copy of this rank's rows ----
     e2e = None
     if not args.no_e2e:
@@ -585,6 +570,22 @@ def run_ours(args, rank, world, dist):
         ingest["upload_s"] = statistics.median(up_s[1:])
         ingest["upload_GBps"] = A_local.nbytes / ingest["upload_s"] / 1e9
         del A_local
+
+    # ---- CPU baseline (rank 0, N=1), after the GPU measurements: OpenBLAS's
+    # spinning worker threads would otherwise steal the cores of the e2e upload ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        smp = CpuSample(W, A_host, sample_rows=args.sample_rows)
+        v, desc, dt = smp.run()
+        cpu = {"value": v, "unit": UNIT, "cores": blas_threads(), "kind": "port",
+               "sample": desc, "seconds": dt}
+        del smp
+        if converged is not None:
+            from oracle.restarted import restarted_oracle
+
+            t0 = time.perf_counter()
+            restarted_oracle(A_host, 10, 30, tol=1e-10, seed=W["seed"])
+            converged["cpu_port_ms"] = 1e3 * (time.perf_counter() - t0)
 
     if rank == 0:
         line = {

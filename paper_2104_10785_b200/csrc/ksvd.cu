@@ -14,6 +14,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <chrono>
@@ -1407,8 +1409,10 @@ static bool pread_all(int fd, void* buf, size_t bytes, off_t off) {
   }
   return true;
 }
-// Page-cache copies are bound by one core's memcpy (~6 GB/s); split each
-// chunk across io threads (KSVD_IO_THREADS, default min(8, cores)).
+// Page-cache and pageable-memory copies are bound by one core's memcpy
+// (~6 GB/s); split each chunk across io threads (KSVD_IO_THREADS, default
+// min(8, cores): 37-44 GB/s uploads, 16 threads measured no faster) of a persistent pool -- spawning the threads per chunk
+// cost more than the copy for small transfers.
 static int io_threads() {
   static const int v = [] {
     const char* e = getenv("KSVD_IO_THREADS");
@@ -1417,19 +1421,78 @@ static int io_threads() {
   }();
   return v;
 }
+
+class IoPool {
+ public:
+  explicit IoPool(int n) {
+    for (int t = 0; t < n; ++t) th_.emplace_back([this, t] { work(t); });
+  }
+  ~IoPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& x : th_) x.join();
+  }
+  // run job(t) for t in [0, n) on the pool (n <= size), caller waits
+  template <class J>
+  void run(int n, J&& job) {
+    std::lock_guard<std::mutex> serial(run_mu_);  // one job at a time
+    std::unique_lock<std::mutex> lk(mu_);
+    job_ = [&job](int t) { job(t); };
+    njob_ = n;
+    pending_ = n;
+    ++gen_;
+    cv_.notify_all();
+    done_cv_.wait(lk, [this] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+  int size() const { return (int)th_.size(); }
+
+ private:
+  void work(int t) {
+    unsigned long long seen = 0;
+    for (;;) {
+      std::function<void(int)> job;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        if (t >= njob_) continue;
+        job = job_;
+      }
+      job(t);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) done_cv_.notify_all();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex mu_, run_mu_;
+  std::condition_variable cv_, done_cv_;
+  std::function<void(int)> job_;
+  int njob_ = 0, pending_ = 0;
+  unsigned long long gen_ = 0;
+  bool stop_ = false;
+};
+
+static IoPool& io_pool() {
+  static IoPool pool(io_threads());
+  return pool;
+}
+
 template <class F>
 static bool io_parallel(size_t bytes, F&& part) {
   const size_t grain = 1 << 20;
   const int T = (int)std::min<size_t>((size_t)io_threads(), (bytes + grain - 1) / grain);
   if (T <= 1) return part((size_t)0, bytes);
   const size_t step = ((bytes + T - 1) / T + 4095) & ~(size_t)4095;
-  std::vector<std::thread> th;
   std::vector<char> ok(T, 0);
-  for (int t = 0; t < T; ++t) {
+  io_pool().run(T, [&](int t) {
     const size_t lo = std::min(bytes, (size_t)t * step), hi = std::min(bytes, lo + step);
-    th.emplace_back([&, t, lo, hi] { ok[t] = part(lo, hi - lo); });
-  }
-  for (auto& x : th) x.join();
+    ok[t] = part(lo, hi - lo) ? 1 : 0;
+  });
   for (char o : ok)
     if (!o) return false;
   return true;
