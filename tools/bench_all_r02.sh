@@ -1,7 +1,7 @@
 #!/bin/bash
 # every BASELINE config through bench.py (our arm + the reference arm), one GPU
 cd "${GRAFT_REPO_ROOT:-.}"
-O=gpurun_out/r02_all; mkdir -p $O
+O=${BENCH_OUT:-gpurun_out/r02_all}; mkdir -p $O
 for c in 1 2 3 5 4; do
   timeout 1200 python bench.py --config $c --steps 10 --warmup 3 > $O/ours_c$c.json 2> $O/ours_c$c.err
   echo "config $c rc=$?" >> $O/rc.txt
