@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "gen.cuh"
+#include "pair.cuh"
 #include "kernels.cuh"
 #include "klrm.cuh"
 #include "resident.cuh"
@@ -951,6 +952,49 @@ static int cgs_tile_multi(ksvd_ctx* c, CgsWork* W, const double* B, int64_t ldb,
                 (const double*)W->c, eps, slot, st, step, code, hp, side);
 }
 
+// ---- both CGS2 of a step in one kernel (k_cgs2_pair, pair.cuh) ----
+struct PairGeom {
+  int64_t G[2] = {0, 0}, rows[2] = {0, 0};
+  size_t smem = 0;
+  int maxe = 0;
+  bool ok = false;
+};
+static PairGeom pair_geom(const ksvd_ctx* c, int64_t L0, int64_t L1, int ncols) {
+  PairGeom g;
+  const int64_t Gt = c->sms;
+  if (L0 <= 0 || L1 <= 0 || ncols <= 0 || Gt < 2) return g;
+  // CTAs in proportion to the rows (equal rows per CTA on both sides), at
+  // least 32 rows per CTA (k_cgs2_tile2's rule)
+  int64_t G0 = std::llround((double)Gt * (double)L0 / (double)(L0 + L1));
+  G0 = std::min<int64_t>(std::max<int64_t>(G0, 1), Gt - 1);
+  const int64_t L[2] = {L0, L1};
+  const int64_t Gs[2] = {G0, Gt - G0};
+  for (int s = 0; s < 2; ++s) {
+    int64_t Gi = std::min<int64_t>(Gs[s], std::max<int64_t>(1, cdiv(L[s], 32)));
+    g.rows[s] = rup(cdiv(L[s], Gi), 2);
+    g.G[s] = cdiv(L[s], g.rows[s]);
+  }
+  const int64_t rmax = std::max(g.rows[0], g.rows[1]);
+  g.smem = sizeof(double) * ((size_t)ncols * (size_t)rmax + 2 * (size_t)(ncols + 1)) + 16;
+  g.maxe = (int)cdiv(rmax, 32);
+  g.ok = rmax <= 256 && g.smem <= kTileSmemMax && g.G[0] + g.G[1] <= c->sms;
+  return g;
+}
+// KSVD_PAIR=0 restores the serialised step (two CGS2 kernels).
+static bool pair_enabled(const ksvd_ctx* c, const ksvd_mat* M) {
+  static const bool off = [] {
+    const char* e = getenv("KSVD_PAIR");
+    return e && strcmp(e, "0") == 0;
+  }();
+  return !off && c->comm == nullptr && !M->fac && M->mloc > 0;
+}
+
+template <int MAXE>
+static const void* pair_kernel(int device) {
+  const void* k = (const void*)k_cgs2_pair<MAXE>;
+  return smem_attr(k, device, (int)kTileSmemMax) == 0 ? k : nullptr;
+}
+
 // ---------------------------------------------------------------------------
 // runs
 constexpr int kLag = 3;   // steps enqueued ahead of the last completed one
@@ -969,6 +1013,7 @@ struct ksvd_run {
   CgsWork left, right;
   double* slot = nullptr;  // scratch scalars
   int kprime = 0, flags = 0, status = 0;
+  bool pair_prev = false;  // the last step was paired: p_i is normalised in P[:, i-1]
   // Ritz
   double *G = nullptr, *V = nullptr, *U = nullptr, *sig = nullptr;
 };
@@ -1015,6 +1060,97 @@ static void free_run(ksvd_run* R) {
 static double* Qcol(ksvd_run* R, int j) { return R->Q + (int64_t)j * R->ldq; }
 static double* Pcol(ksvd_run* R, int j) { return R->P + (int64_t)j * R->ldp; }
 
+// CGS2 of w against Q[:, :i] and of y = A^T w (the split partials of the
+// last k_gemv_t2) against P[:, :i]; beta_{i+1}, alpha_{i+1}, q_{i+1} -> Q[:, i],
+// p_{i+1} -> P[:, i], breakdown status -- one launch.
+static int cgs_pair(ksvd_run* R, int i, const PairGeom& g) {
+  ksvd_mat* M = R->M;
+  ksvd_ctx* c = M->ctx;
+  PairArgs a{};
+  CgsWork* W[2] = {&R->left, &R->right};
+  const double* B[2] = {R->Q, R->P};
+  const int64_t ldb[2] = {R->ldq, R->ldp};
+  const int64_t L[2] = {M->mloc, M->n};
+  double* out[2] = {Qcol(R, i), Pcol(R, i)};
+  for (int s = 0; s < 2; ++s) {
+    TRY(ensure_cgs(c->stream, W[s], g.G[s], 2 * (i + 1)));
+    PairSide& S = a.s[s];
+    S.B = B[s];
+    S.ldb = ldb[s];
+    S.ncols = i;
+    S.L = L[s];
+    S.rows = (int)g.rows[s];
+    S.G = (int)g.G[s];
+    S.part = W[s]->part;
+    S.c = W[s]->c;
+    S.out = out[s];
+  }
+  a.s[0].x = R->w;
+  a.s[1].fpart = M->part_t;
+  a.s[1].fld = M->n_pad;
+  a.s[1].fnsplit = (int)M->pt.nsplit;
+  a.passes = R->reorth;
+  a.eps = R->eps;
+  a.beta_slot = R->beta + i + 1;
+  a.alpha_slot = R->alpha + i + 1;
+  a.st = R->st;
+  a.step = i;
+  a.hp = c->dprog;
+  const int64_t G = g.G[0] + g.G[1];
+  static const int64_t red_max = [] {
+    const char* e = getenv("KSVD_RED_MAX");
+    return e ? (int64_t)atoll(e) : (int64_t)148 * 16;
+  }();
+  a.redundant = std::max(g.G[0], g.G[1]) <= 160 && (int64_t)(i + 1) * G <= red_max;
+  const void* kern = nullptr;
+  switch (g.maxe) {
+    case 1: kern = pair_kernel<1>(c->device); break;
+    case 2: kern = pair_kernel<2>(c->device); break;
+    case 3: kern = pair_kernel<3>(c->device); break;
+    case 4: kern = pair_kernel<4>(c->device); break;
+    case 5: kern = pair_kernel<5>(c->device); break;
+    case 6: kern = pair_kernel<6>(c->device); break;
+    case 7: kern = pair_kernel<7>(c->device); break;
+    default: kern = pair_kernel<8>(c->device); break;
+  }
+  if (!kern) return set_err(KSVD_ERUNTIME, "k_cgs2_pair: shared-memory attribute");
+  const bool reg = !c->coop_cgs;
+  a.bar = reg ? R->left.bar : nullptr;
+  void* args[] = {&a};
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->profiling) {
+    TRY(get_event(c, &e0));
+    TRY(get_event(c, &e1));
+    CK(cudaEventRecord(e0, c->stream));
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)G);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = g.smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (!reg) {
+    at[na].id = cudaLaunchAttributeCooperative;
+    at[na].val.cooperative = 1;
+    ++na;
+  }
+  if (pdl_enabled(c)) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  CK(cudaLaunchKernelExC(&cfg, kern, args));
+  if (c->profiling) {
+    CK(cudaEventRecord(e1, c->stream));
+    c->pending.push_back({e0, e1, KC_CGS});
+  }
+  c->launches++;
+  return 0;
+}
+
 // One GK iteration i (1-based), bidiag.py:151-178.
 // host-side enqueue timing per section (KSVD_DEBUG_HOST)
 static double g_tsec[6];
@@ -1035,13 +1171,30 @@ static int enqueue_step(ksvd_run* R, int i) {
     TRY(grow_bases(R, i + 1 <= R->k_max ? i + 1 : i));
   }
   SecTimer t_all(5);
+  // paired step (pair.cuh): A^T runs on the finalised w, then ONE kernel
+  // orthogonalises both sides
+  PairGeom pg;
+  if (i < R->k_max && pair_enabled(c, M)) pg = pair_geom(c, M->mloc, M->n, i);
   // w = A p_i - alpha_i q_i, with p_i = z / alpha_i stored to P[:, i-1]
+  // (after a paired step p_i is already there, normalised)
   {
     SecTimer t(1);
-    TRY(enqueue_gemv_n(M, R->z, R->alpha + i, Pcol(R, i - 1), Qcol(R, i - 1), R->alpha + i,
-                       R->w, R->st, i,
-                       /*finalize=*/!coop_enabled(c, M->mloc, i, true) &&
-                           !multi_tile_enabled(c, M->mloc, i)));
+    const bool fin = pg.ok || (!coop_enabled(c, M->mloc, i, true) &&
+                               !multi_tile_enabled(c, M->mloc, i));
+    if (R->pair_prev)
+      TRY(enqueue_gemv_n(M, Pcol(R, i - 1), nullptr, nullptr, Qcol(R, i - 1), R->alpha + i,
+                         R->w, R->st, i, fin));
+    else
+      TRY(enqueue_gemv_n(M, R->z, R->alpha + i, Pcol(R, i - 1), Qcol(R, i - 1), R->alpha + i,
+                         R->w, R->st, i, fin));
+  }
+  R->pair_prev = false;
+  if (pg.ok) {
+    TRY(dense_gemv_t(M, R->w, nullptr, nullptr, nullptr, nullptr, R->z, R->st, i, true,
+                     /*finalize=*/false));
+    TRY(cgs_pair(R, i, pg));
+    R->pair_prev = true;
+    return 0;
   }
   SecTimer t_cgs(2);
   // CGS2 against Q[:, :i]; beta_{i+1} = ||w||; beta < eps -> breakdown
@@ -1159,6 +1312,7 @@ static int run_steps(ksvd_run* R, int i0) {
   static const bool dbg = getenv("KSVD_DEBUG_HOST") != nullptr;
   using clk = std::chrono::steady_clock;
   double t_launch = 0, t_wait = 0;
+  R->pair_prev = false;  // callers leave z = A^T q_{i0} unnormalised
   for (int i = i0; i <= R->k_max; ++i) {
     auto t0 = clk::now();
     if (i - i0 >= kLag) {
