@@ -146,6 +146,21 @@ __device__ __forceinline__ double strided_sum(const double* __restrict__ p, int6
   return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
+// strided_sum with 8 loads in flight (the same fixed order, so the same
+// bits): for kernels that cannot spare strided_sum's registers
+__device__ __forceinline__ double strided_sum8(const double* __restrict__ p, int64_t ld,
+                                               int cnt) {
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int k = 0; k < cnt; k += 8) {
+    double t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t[u] = k + u < cnt ? __ldcg(p + (int64_t)(k + u) * ld) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u & 3] += t[u];
+  }
+  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
 // ---------------------------------------------------------------------------
 // 16-byte streaming loads of A.  A is read exactly once per pass, so it is
 // loaded through the non-coherent path without L1 allocation.
@@ -204,12 +219,24 @@ __device__ __forceinline__ double ldv(const double* p) {
 // read last stay in L2 for k_gemv_t2, which sweeps up).  Partials go to
 // part[group * m + row]; k_gemv_n_finalize (or the CGS2 kernels' fused
 // finalisation) adds them in group order and applies - alpha q.
-template <typename TA, int U>
+// FIN (the paired step, pair.cuh): the last CTA of each row segment to
+// finish (an arrival counter per segment, reset by that CTA) adds the
+// segment's chunk-group partials in group order and writes
+// w = A p - (*nalpha) qprev -- k_gemv_n_finalize's arithmetic, in the
+// product's tail instead of a launch of its own.
+struct GemvNFin {
+  unsigned* seg_cnt;  // nseg zero-initialised counters
+  const double* qprev;
+  const double* nalpha;
+  double* w;
+};
+
+template <typename TA, int U, bool FIN>
 __global__ void __launch_bounds__(kThreads)
 k_gemv_n(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nchunks,
           int ngroups, int64_t nseg, const double* __restrict__ p_src,
           const double* __restrict__ p_scale, double* __restrict__ p_dst, int64_t n_true,
-          double* __restrict__ part, const DevState* st) {
+          double* __restrict__ part, const DevState* st, GemvNFin fin) {
   pdl_wait();
   pdl_trigger(1);
   if (halted(st)) return;
@@ -271,6 +298,29 @@ k_gemv_n(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nch
       for (int w = 1; w < kWarps; ++w) sum += red[par][w][lane];
       const int64_t row = r + lane;
       if (row < m) part[(int64_t)grp * m + row] = sum;
+    }
+  }
+  if constexpr (FIN) {
+    __shared__ int last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last = atomicAdd(fin.seg_cnt + rseg, 1u) == (unsigned)ngroups - 1;
+      if (last) {
+        fin.seg_cnt[rseg] = 0;  // ready for the next launch
+        __threadfence();
+      }
+    }
+    __syncthreads();
+    if (!last) return;
+    const double al = __ldcg(fin.nalpha);
+    // the segment's rows: rseg*8 + k*nseg*8 + j (j < 8)
+    const int64_t nblk = (m - rseg * 8 + nseg * 8 - 1) / (nseg * 8);
+    for (int64_t t = threadIdx.x; t < nblk * 8; t += kThreads) {
+      const int64_t row = rseg * 8 + (t >> 3) * nseg * 8 + (t & 7);
+      if (row >= m) continue;
+      const double s = strided_sum8(part + row, m, ngroups);
+      fin.w[row] = s - al * __ldcg(fin.qprev + row);
     }
   }
 }

@@ -293,6 +293,7 @@ struct ksvd_mat {
   GemvNPlan pn{};
   GemvTPlan pt{};
   double* part_n = nullptr;  // ngroups x mloc: k_gemv_n partial row sums
+  unsigned* seg_cnt = nullptr;  // nseg arrival counters (k_gemv_n<FIN>)
   double* part_t = nullptr;  // nsplit x n_pad
   // plain-product scratch
   double *dx = nullptr, *dy = nullptr;
@@ -314,7 +315,7 @@ static size_t esize(int dtype) { return dtype == KSVD_F32 ? 4 : 8; }
 
 template <typename TA>
 static int occupancy_n(int* out) {
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k_gemv_n<TA, kUnrollN>, kThreads, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k_gemv_n<TA, kUnrollN, false>, kThreads, 0));
   return 0;
 }
 
@@ -378,6 +379,8 @@ static int alloc_matrix_buffers(ksvd_mat* M) {
   CK(cudaMallocAsync((void**)&M->part_n,
                      sizeof(double) * M->pn.ngroups * std::max<int64_t>(M->mloc, 1), s));
   CK(cudaMallocAsync((void**)&M->part_t, sizeof(double) * M->pt.nsplit * M->n_pad, s));
+  CK(cudaMallocAsync((void**)&M->seg_cnt, sizeof(unsigned) * M->pn.nseg, s));
+  CK(cudaMemsetAsync(M->seg_cnt, 0, sizeof(unsigned) * M->pn.nseg, s));
   CK(cudaMallocAsync((void**)&M->dx, vec, s));
   CK(cudaMallocAsync((void**)&M->dy, vec, s));
   CK(cudaMemsetAsync(M->dx, 0, vec, s));
@@ -400,7 +403,7 @@ static int free_matrix(ksvd_mat* M) {
     M->fac = nullptr;
   }
   for (void* p : {(void*)M->A, (void*)M->part_n, (void*)M->part_t, (void*)M->dx, (void*)M->dy,
-                  (void*)M->st0})
+                  (void*)M->st0, (void*)M->seg_cnt})
     if (p) cudaFreeAsync(p, s);
   cudaFree(M->gen_ps);
   cudaFree(M->gen_q);
@@ -411,21 +414,27 @@ static int free_matrix(ksvd_mat* M) {
 // w = A p (- alpha q): partial row sums per chunk group (k_gemv_n), then
 // the group sums + epilogue (k_gemv_n_finalize) unless the caller fuses the
 // finalisation into its k_cgs2_* launch (finalize = false).
+// tail_fin (the paired step): the finalisation runs in k_gemv_n's tail
+// (FIN instantiation, per-segment arrival counters M->seg_cnt) instead.
 static int dense_gemv_n(ksvd_mat* M, const double* p_src, const double* p_scale,
                         double* p_dst, const double* qprev, const double* alpha,
-                        double* w, DevState* st, int step, bool finalize = true) {
+                        double* w, DevState* st, int step, bool finalize = true,
+                        bool tail_fin = false) {
   ksvd_ctx* c = M->ctx;
   const GemvNPlan& pn = M->pn;
   if (M->mloc == 0) return 0;
   const dim3 grid((unsigned)pn.blocks);
+  const GemvNFin nf{M->seg_cnt, qprev, alpha, w};
+#define KSVD_GN(TA, F)                                                                      \
+  launch_step(c, KC_GEMV_N, k_gemv_n<TA, kUnrollN, F>, grid, dim3(kThreads), 0,              \
+              (const TA*)M->A, M->lda, M->mloc, pn.nvec, pn.nchunks, pn.ngroups, pn.nseg,    \
+              p_src, p_scale, p_dst, M->n, M->part_n, (const DevState*)st, nf)
   if (M->dtype == KSVD_F32)
-    TRY(launch_step(c, KC_GEMV_N, k_gemv_n<float, kUnrollN>, grid, dim3(kThreads), 0,
-                    (const float*)M->A, M->lda, M->mloc, pn.nvec, pn.nchunks, pn.ngroups,
-                    pn.nseg, p_src, p_scale, p_dst, M->n, M->part_n, (const DevState*)st));
+    TRY(tail_fin ? KSVD_GN(float, true) : KSVD_GN(float, false));
   else
-    TRY(launch_step(c, KC_GEMV_N, k_gemv_n<double, kUnrollN>, grid, dim3(kThreads), 0,
-                    (const double*)M->A, M->lda, M->mloc, pn.nvec, pn.nchunks, pn.ngroups,
-                    pn.nseg, p_src, p_scale, p_dst, M->n, M->part_n, (const DevState*)st));
+    TRY(tail_fin ? KSVD_GN(double, true) : KSVD_GN(double, false));
+#undef KSVD_GN
+  if (tail_fin) return 0;
   if (finalize)
     TRY(launch(c, KC_FIN, k_gemv_n_finalize, dim3((unsigned)cdiv(M->mloc, kThreads)),
                dim3(kThreads), 0, (const double*)M->part_n, M->mloc, pn.ngroups, M->mloc,
@@ -1181,12 +1190,20 @@ static int enqueue_step(ksvd_run* R, int i) {
     SecTimer t(1);
     const bool fin = pg.ok || (!coop_enabled(c, M->mloc, i, true) &&
                                !multi_tile_enabled(c, M->mloc, i));
-    if (R->pair_prev)
-      TRY(enqueue_gemv_n(M, Pcol(R, i - 1), nullptr, nullptr, Qcol(R, i - 1), R->alpha + i,
-                         R->w, R->st, i, fin));
+    // paired: w finalised in k_gemv_n's tail (KSVD_TAILFIN=0: its own kernel)
+    static const bool tail_off = [] {
+      const char* e = getenv("KSVD_TAILFIN");
+      return e && strcmp(e, "0") == 0;
+    }();
+    const double* p_src = R->pair_prev ? Pcol(R, i - 1) : R->z;
+    const double* p_scale = R->pair_prev ? nullptr : R->alpha + i;
+    double* p_dst = R->pair_prev ? nullptr : Pcol(R, i - 1);
+    if (pg.ok)
+      TRY(dense_gemv_n(M, p_src, p_scale, p_dst, Qcol(R, i - 1), R->alpha + i, R->w, R->st, i,
+                       true, /*tail_fin=*/!tail_off));
     else
-      TRY(enqueue_gemv_n(M, R->z, R->alpha + i, Pcol(R, i - 1), Qcol(R, i - 1), R->alpha + i,
-                         R->w, R->st, i, fin));
+      TRY(enqueue_gemv_n(M, p_src, p_scale, p_dst, Qcol(R, i - 1), R->alpha + i, R->w, R->st, i,
+                         fin));
   }
   R->pair_prev = false;
   if (pg.ok) {

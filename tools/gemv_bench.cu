@@ -16,7 +16,7 @@ float time_n(const TA* A, int64_t lda, int64_t m, int64_t n, const double* p, do
   const int64_t nvec = (n + V - 1) / V;
   const int nchunks = (int)((nvec + 32 * U - 1) / (32 * U));
   const int ngroups = (nchunks + 7) / 8;
-  auto k = k_gemv_n<TA, U>;
+  auto k = k_gemv_n<TA, U, false>;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, 0);
   const int per_sm = occ < ctas_per_sm ? occ : ctas_per_sm;
@@ -30,7 +30,7 @@ float time_n(const TA* A, int64_t lda, int64_t m, int64_t n, const double* p, do
   for (int r = 0; r < 10; ++r) {
     cudaEventRecord(a);
     k<<<(unsigned)blocks, 256>>>(A, lda, m, nvec, nchunks, ngroups, nseg, p, nullptr, nullptr, n,
-                                 part, st);
+                                 part, st, GemvNFin{});
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms;
