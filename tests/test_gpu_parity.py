@@ -289,6 +289,7 @@ _MULTI = {"KSVD_RESIDENT": "0"}  # small cases would otherwise take the resident
                                  {"KSVD_RED_MAX": "0", **_MULTI},
                                  {"KSVD_RED_MAX": "100000000", **_MULTI}, {"KSVD_PDL": "0", **_MULTI},
                                  {"KSVD_FORCE_COOP": "1", **_MULTI},
+                                 {"KSVD_PAIR": "0", **_MULTI}, {"KSVD_TAILFIN": "0", **_MULTI},
                                  _MULTI, {}])
 def test_cgs_paths_agree(env):
     """The whole-loop resident kernel (small matrices, default), the
@@ -299,7 +300,10 @@ def test_cgs_paths_agree(env):
     when the residency probe fails); KSVD_FORCE_NCCL runs the multi-rank code
     path (NCCL all-reduces between the kernels, k_cgs_tile_phase) over a
     1-rank communicator, KSVD_FORCE_PX the same path with every all-reduce
-    through the NVLink peer-exchange kernel (csrc/peer.cuh) instead."""
+    through the NVLink peer-exchange kernel (csrc/peer.cuh) instead.
+    _MULTI takes the paired step (both CGS2 in k_cgs2_pair, pair.cuh) where
+    its tiles fit; KSVD_PAIR=0 the serialised step, KSVD_TAILFIN=0 the paired
+    step with a separate w finalisation kernel."""
     import json
     import os
     import subprocess
@@ -312,3 +316,27 @@ def test_cgs_paths_agree(env):
     assert res.returncode == 0, res.stderr[-2000:]
     for rel, cos, rank, l in json.loads(res.stdout.strip().splitlines()[-1]):
         assert rel <= SIG_RTOL_F64 and cos >= 1 - COS_TOL_F64 and rank == l, (env, rel, cos, rank)
+
+
+def test_paired_step_is_three_launches_and_matches_oracle():
+    """The paired step (pair.cuh): k_gemv_n (w finalised in its tail),
+    k_gemv_t2 on w, ONE k_cgs2_pair -- 3 launches per GK step -- and the
+    bidiagonalization still meets the parity bar against the oracle."""
+    from paper_2104_10785_b200 import _lib
+
+    # 48 MB: not the resident kernel; rank 60, no breakdown within 40 steps
+    A = synth.low_rank_synth(4000, 1500, 60, seed=12)
+    op = K.DeviceMatrix.from_host(A)
+    ctx = _lib.get_context()
+    counts = {}
+    for k in (20, 40):
+        n0 = ctx.launch_count()
+        K.bidiagonalize(op, K.BidiagConfig(k_max=k, seed=12))
+        counts[k] = ctx.launch_count() - n0
+    assert (counts[40] - counts[20]) == 3 * 20, counts
+    ps = K.fsvd(op, k=80, r=20, cfg=K.BidiagConfig(k_max=80, seed=12))
+    ref = O.fsvd_oracle(A, 80, 20, seed=12)
+    assert np.max(np.abs(ps.sigma - ref.sigma) / ref.sigma) <= SIG_RTOL_F64
+    cos = min(np.min(np.abs(np.einsum("ij,ij->j", ps.U, ref.U))),
+              np.min(np.abs(np.einsum("ij,ij->j", ps.V, ref.V))))
+    assert cos >= 1 - COS_TOL_F64
