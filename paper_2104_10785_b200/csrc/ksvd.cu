@@ -1843,7 +1843,13 @@ static int run_resident(ksvd_run* Rn, const ResidentPlan& pl, const double* q1_l
   a.w_out = Rn->w;
   a.st = Rn->st;
   a.tdbg = c->tdbg;
-  const size_t part_elems = 2 * (((size_t)(a.kq + 1) * pl.G + 1) & ~(size_t)1) + 2;
+  // paired step (KSVD_RES_PAIR=0: the serialised 6-round step)
+  static const bool res_pair_off = [] {
+    const char* e = getenv("KSVD_RES_PAIR");
+    return e && strcmp(e, "0") == 0;
+  }();
+  a.paired = (!res_pair_off && Rn->reorth == 2) ? 1 : 0;
+  const size_t part_elems = 4 * (((size_t)(a.kq + 1) * pl.G + 1) & ~(size_t)1) + 2;
   const size_t z_elems = (size_t)pl.G * M->n;
   double* buf = nullptr;
   CK(cudaMallocAsync(&buf, sizeof(double) * (M->n_pad + part_elems + z_elems), s));

@@ -13,7 +13,15 @@
 //   z partials over the CTA's rows for all n columns  -> 1 round
 //   z chunk = sum of the partials - beta p (fixed order)
 //   CGS2 of z against P (2 rounds), alpha, publish p   -> 1 round
-// i.e. 6 grid barriers per step.  Semantics, scalars, breakdown codes and
+// i.e. 6 grid barriers per step.  The paired step (a.paired, the arithmetic
+// of pair.cuh: A^T runs on the finalised w before its CGS2, both CGS2 share
+// grid rounds, alpha = ||y'|| / beta) needs 4:
+//   w = A p - alpha q; z partials of A^T w and the left pass-1 dots -> 1 round
+//   left update + pass-2 dots (+ norm); z chunk; right pass-1 dots    -> 1 round
+//   left update, beta, q; right update + pass-2 dots (+ norm)         -> 1 round
+//   right update, alpha, publish p                                    -> 1 round
+// (plus a direct-norm round where the closed form would cancel).
+// Semantics, scalars, breakdown codes and
 // the residual left in R->w are those of the multi-kernel loop
 // (bidiag.py:111-178), so ksvd_run_info / _extend / _ritz work unchanged.
 #pragma once
@@ -35,8 +43,9 @@ struct ResArgs {
   double *alpha, *beta;  // 1-based
   double* w_out;         // residual at a beta breakdown (ksvd_run_extend)
   double* pvec;          // current p (n)
-  double* part;          // CGS partials: 2 x (kq + 1) x G
+  double* part;          // CGS partials: 4 x (kq + 1) x G (even-rounded blocks)
   double* zpart;         // gemv_t partials: G x n
+  int paired;            // the paired step (pair.cuh's arithmetic, 4 grid rounds)
   DevState* st;
   unsigned long long* tdbg;  // KSVD_PHASE_TIMES: CTA-0 phase times (nullable)
 };
@@ -247,6 +256,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_gk_resident(ResArgs a) {
   if (b == 0 && tid == 0) a.alpha[l + 1] = alpha;
   publish_p(l, alpha);
 
+  const int64_t hblk = ((int64_t)(a.kq + 1) * G + 1) & ~(int64_t)1;
+  double* const PL0 = a.part;             // paired step: left / right partial blocks
+  double* const PL1 = a.part + hblk;
+  double* const PR0 = a.part + 2 * hblk;
+  double* const PR1 = a.part + 3 * hblk;
+  // ||c||^2 of red[0:ncols] (the same fixed order in every warp of every CTA)
+  auto ccnorm = [&](int ncols) {
+    double cc = 0.0;
+    for (int j = (int)(threadIdx.x & 31); j < ncols; j += 32) cc = fma(red[j], red[j], cc);
+    return warp_sum(cc);
+  };
+
   for (int i = l + 1; i <= a.k_max; ++i) {
     // w = A p_i - alpha_i q_i (bidiag.py:152); p staged in shared memory
     bulk(pv, a.pvec, (uint32_t)(((n + 1) & ~(int64_t)1) * sizeof(double)));
@@ -259,6 +280,79 @@ __global__ void __launch_bounds__(kThreads, 1) k_gk_resident(ResArgs a) {
     }
     __syncthreads();
     mark(1);
+    if (a.paired && i < a.k_max) {
+      // [round 1] y partials = A^T w over this CTA's rows; left pass-1 dots
+      {
+        double* zp = a.zpart + (int64_t)b * n;
+        for (int64_t c = tid; c < n; c += kThreads) {
+          double s = 0.0;
+          for (int r = 0; r < nr; ++r) s = fma((double)As[(int64_t)r * n + c], wv[r], s);
+          zp[c] = s;
+        }
+      }
+      dots(Qs, R, i, wv, nr, PL0, false);
+      grid.sync();
+      // [round 2] left update + pass-2 dots and norm; y chunk; right pass-1 dots
+      reduce(PL0, 0, i);
+      update(Qs, R, i, wv, nr);
+      dots(Qs, R, i, wv, nr, PL1, true);
+      for (int cc = warp; cc < nc; cc += kWarps) {
+        double s = 0.0;
+        for (int q = lane; q < G; q += 32) s += __ldcg(a.zpart + (int64_t)q * n + c0 + cc);
+        s = warp_sum(s);
+        if (lane == 0) zv[cc] = s;
+      }
+      __syncthreads();
+      dots(Ps, C, i, zv, nc, PR0, false);
+      grid.sync();
+      // [round 3] left update, beta (closed form); right update + pass-2 dots
+      reduce(PL1, 0, i + 1);
+      const double ccl = ccnorm(i), nnl = red[i];
+      update(Qs, R, i, wv, nr);
+      const bool dir_l = !(ccl <= 1e-6 * nnl);
+      reduce(PR0, 0, i);
+      update(Ps, C, i, zv, nc);
+      dots(Ps, C, i, zv, nc, PR1, true);
+      if (dir_l) dots(Qs, R, 0, wv, nr, PL0, true);  // direct norm (rare)
+      grid.sync();
+      double n2l = nnl - ccl;
+      if (dir_l) {
+        reduce(PL0, 0, 1);
+        n2l = red[0];
+      }
+      const double beta = sqrt(n2l);
+      if (!isfinite(beta)) return finish(ST_NONFINITE, i);
+      if (b == 0 && tid == 0) a.beta[i + 1] = beta;
+      if (beta < a.eps) {  // bidiag.py:158-164: the residual stays for _terminal_column
+        for (int r = tid; r < nr; r += kThreads) a.w_out[r0 + r] = wv[r];
+        return finish(ST_BETA_BREAK, i);
+      }
+      for (int r = tid; r < nr; r += kThreads) {
+        const double v = wv[r] / beta;
+        Qs[(size_t)i * R + r] = v;
+        a.Q[(int64_t)i * a.ldq + r0 + r] = v;
+      }
+      // [round 4] right update, alpha = ||y'|| / beta, publish p = y' / ||y'||
+      reduce(PR1, 0, i + 1);
+      const double ccr = ccnorm(i), nnr = red[i];
+      update(Ps, C, i, zv, nc);
+      double n2r = nnr - ccr;
+      if (!(ccr <= 1e-6 * nnr)) {  // direct norm (rare): one more round
+        dots(Ps, C, 0, zv, nc, PR0, true);
+        grid.sync();
+        reduce(PR0, 0, 1);
+        n2r = red[0];
+      }
+      const double ynrm = sqrt(n2r);
+      alpha = ynrm / beta;
+      if (!isfinite(alpha)) return finish(ST_NONFINITE, i);
+      if (b == 0 && tid == 0) a.alpha[i + 1] = alpha;
+      if (alpha < a.eps) return finish(ST_ALPHA_BREAK, i);
+      // p = y' / ||y'|| (publish_p divides its zv by the scale it is given)
+      publish_p(i, ynrm);
+      mark(5);
+      continue;
+    }
     nrm2 = cgs2(Qs, R, i, wv, nr);
     mark(2);
     const double beta = sqrt(nrm2);
