@@ -1183,7 +1183,9 @@ static int enqueue_step(ksvd_run* R, int i) {
   // paired step (pair.cuh): A^T runs on the finalised w, then ONE kernel
   // orthogonalises both sides
   PairGeom pg;
-  if (i < R->k_max && pair_enabled(c, M)) pg = pair_geom(c, M->mloc, M->n, i);
+  // (two CGS passes: the right pass must remove beta^2 p_i and A^T Q d, which a
+  // single classical pass against a not quite orthonormal basis leaves behind)
+  if (i < R->k_max && R->reorth == 2 && pair_enabled(c, M)) pg = pair_geom(c, M->mloc, M->n, i);
   // w = A p_i - alpha_i q_i, with p_i = z / alpha_i stored to P[:, i-1]
   // (after a paired step p_i is already there, normalised)
   {

@@ -27,6 +27,9 @@
 // The reductions of both sides run in the same grid rounds: 2 rounds for
 // the pair (redundant reductions: every CTA sums both sides' partials) or 4
 // (distributed column sums), instead of 2 x (2 or 4) for two kernels.
+// Used with two CGS passes only (reorth_passes=2, the default): one classical
+// pass against a basis that is orthonormal only to working precision would
+// leave a fraction of beta^2 p_i and A^T Q d behind.
 // Every CTA ends with both reduced coefficient vectors, so the closed-form
 // norm test (||x||^2 - ||c||^2, a direct-norm round where it would cancel)
 // is decided identically everywhere.

@@ -124,3 +124,31 @@ def test_nan_and_inf_raise_numerical_error():
         A[17, 33] = bad
         with pytest.raises(K.NumericalError):
             K.estimate_rank(A)
+
+
+def test_golden_and_edges_through_streaming_kernels():
+    """The reference-generated golden cases (breakdowns, degenerate and
+    terminal columns included) and this module's edge cases with the
+    whole-loop resident kernel disabled (KSVD_RESIDENT=0): the small shapes
+    then run the streaming kernels -- the paired step (k_cgs2_pair, pair.cuh)
+    wherever its tiles fit -- in a subprocess (the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    here = Path(__file__).resolve()
+    par = root / "tests" / "test_gpu_parity.py"
+    ids = [f"{par}::{t}" for t in ("test_bidiag_golden", "test_fsvd_golden", "test_rank_golden",
+                                   "test_bidiag_edge_cases", "test_nonfinite_raises",
+                                   "test_spurious_filter_stops_at_rank")]
+    ids += [f"{here}::{t}" for t in ("test_bidiag_shapes_vs_oracle", "test_fsvd_shapes_vs_oracle",
+                                     "test_k_max_one_and_single_pass_reorth",
+                                     "test_large_eps_breaks_down_immediately",
+                                     "test_rank_shapes_and_modes", "test_float32_inputs_everywhere",
+                                     "test_nan_and_inf_raise_numerical_error")]
+    res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                          *ids], cwd=root, env={**os.environ, "KSVD_RESIDENT": "0"},
+                         capture_output=True, text=True, timeout=1200)
+    assert res.returncode == 0, res.stdout[-3000:]
