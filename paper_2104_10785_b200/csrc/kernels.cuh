@@ -231,7 +231,20 @@ struct GemvNFin {
   double* w;
 };
 
-template <typename TA, int U, bool FIN>
+// NB: the CTA-level row sums with named barriers instead of one
+// __syncthreads per 8-row block: warps 1-7 arrive (bar.arrive) on FULL[par]
+// after storing their partials and only wait (EMPTY[par]) if they get two
+// blocks ahead of warp 0, which syncs on FULL[par], sums and stores, then
+// releases EMPTY[par].  Keeps the other warps issuing loads while warp 0
+// reduces.
+__device__ __forceinline__ void nbar_sync(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kThreads) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(kThreads) : "memory");
+}
+
+template <typename TA, int U, bool FIN, bool NB = false>
 __global__ void __launch_bounds__(kThreads)
 k_gemv_n(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nchunks,
           int ngroups, int64_t nseg, const double* __restrict__ p_src,
@@ -268,7 +281,9 @@ k_gemv_n(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nch
   }
   const TA* base = A + ((int64_t)chunk * CW + lane) * V;
   int par = 0;
-  for (int64_t r = rseg * 8; r < m; r += nseg * 8, par ^= 1) {
+  const int64_t niter = rseg * 8 < m ? (m - rseg * 8 + nseg * 8 - 1) / (nseg * 8) : 0;
+  int64_t it = 0;
+  for (int64_t r = rseg * 8; r < m; r += nseg * 8, par ^= 1, ++it) {
     AVec<TA> a[8][U];
 #pragma unroll
     for (int rr = 0; rr < 8; ++rr) {
@@ -290,14 +305,33 @@ k_gemv_n(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nch
       v[rr] = s;
     }
     const double t = warp_sum8(v);
-    if ((lane & 3) == 0) red[par][warp][warp_sum8_index(lane)] = t;
-    __syncthreads();  // red[par] complete; red[par ^ 1] free again (read last round)
-    if (warp == 0 && lane < 8) {
-      double sum = red[par][0][lane];
+    if constexpr (NB) {
+      if (warp != 0 && it >= 2) nbar_sync(3 + par);  // EMPTY[par]: block it-2 consumed
+      if ((lane & 3) == 0) red[par][warp][warp_sum8_index(lane)] = t;
+      if (warp == 0) {
+        nbar_sync(1 + par);  // FULL[par]
+        if (lane < 8) {
+          double sum = red[par][0][lane];
 #pragma unroll
-      for (int w = 1; w < kWarps; ++w) sum += red[par][w][lane];
-      const int64_t row = r + lane;
-      if (row < m) part[(int64_t)grp * m + row] = sum;
+          for (int w = 1; w < kWarps; ++w) sum += red[par][w][lane];
+          const int64_t row = r + lane;
+          if (row < m) part[(int64_t)grp * m + row] = sum;
+        }
+        __syncwarp();
+        if (it + 2 < niter) nbar_arrive(3 + par);
+      } else {
+        nbar_arrive(1 + par);
+      }
+    } else {
+      if ((lane & 3) == 0) red[par][warp][warp_sum8_index(lane)] = t;
+      __syncthreads();  // red[par] complete; red[par ^ 1] free again (read last round)
+      if (warp == 0 && lane < 8) {
+        double sum = red[par][0][lane];
+#pragma unroll
+        for (int w = 1; w < kWarps; ++w) sum += red[par][w][lane];
+        const int64_t row = r + lane;
+        if (row < m) part[(int64_t)grp * m + row] = sum;
+      }
     }
   }
   if constexpr (FIN) {

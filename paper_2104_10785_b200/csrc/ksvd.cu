@@ -425,14 +425,24 @@ static int dense_gemv_n(ksvd_mat* M, const double* p_src, const double* p_scale,
   if (M->mloc == 0) return 0;
   const dim3 grid((unsigned)pn.blocks);
   const GemvNFin nf{M->seg_cnt, qprev, alpha, w};
-#define KSVD_GN(TA, F)                                                                      \
-  launch_step(c, KC_GEMV_N, k_gemv_n<TA, kUnrollN, F>, grid, dim3(kThreads), 0,              \
+  // named-barrier CTA row sums (KSVD_GEMVN_NB=0: one __syncthreads per block);
+  // same box: k_gemv_n 6,396-6,401 -> 6,444-6,449 GB/s on config 4, 6,804-6,823 ->
+  // 6,847-6,855 on config 2 (profiles/r02/gemv_n_nb_ab.txt)
+  static const bool nb = [] {
+    const char* e = getenv("KSVD_GEMVN_NB");
+    return !(e && strcmp(e, "0") == 0);
+  }();
+#define KSVD_GN(TA, F, B)                                                                   \
+  launch_step(c, KC_GEMV_N, k_gemv_n<TA, kUnrollN, F, B>, grid, dim3(kThreads), 0,           \
               (const TA*)M->A, M->lda, M->mloc, pn.nvec, pn.nchunks, pn.ngroups, pn.nseg,    \
               p_src, p_scale, p_dst, M->n, M->part_n, (const DevState*)st, nf)
-  if (M->dtype == KSVD_F32)
-    TRY(tail_fin ? KSVD_GN(float, true) : KSVD_GN(float, false));
-  else
-    TRY(tail_fin ? KSVD_GN(double, true) : KSVD_GN(double, false));
+  if (M->dtype == KSVD_F32) {
+    if (nb) TRY(tail_fin ? KSVD_GN(float, true, true) : KSVD_GN(float, false, true));
+    else TRY(tail_fin ? KSVD_GN(float, true, false) : KSVD_GN(float, false, false));
+  } else {
+    if (nb) TRY(tail_fin ? KSVD_GN(double, true, true) : KSVD_GN(double, false, true));
+    else TRY(tail_fin ? KSVD_GN(double, true, false) : KSVD_GN(double, false, false));
+  }
 #undef KSVD_GN
   if (tail_fin) return 0;
   if (finalize)
