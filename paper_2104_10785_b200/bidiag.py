@@ -114,11 +114,40 @@ class GKRun:
         self._fin()
 
 
+def _host_norm(v: np.ndarray) -> float:
+    """np.linalg.norm (the reference's call) on ONE BLAS thread.  OpenBLAS
+    threads its dot product above 10k elements, and its idle workers then
+    spin for ~0.1 s on every core -- measured: the next staged upload of A
+    (8 host copy threads) ran 2-3x slower (0.8 GB in 44-81 ms instead of
+    17-20 ms).  Single-threaded it is the reference's own result on a
+    one-thread BLAS (below 10k elements, the golden start vectors, it is
+    bit-identical either way)."""
+    lim = _blas_single() if v.size > 8192 else None  # below: never threaded
+    if lim is None:
+        return float(np.linalg.norm(v))
+    with lim.limit(limits=1, user_api="blas"):
+        return float(np.linalg.norm(v))
+
+
+_CTL = []
+
+
+def _blas_single():
+    if not _CTL:
+        try:
+            from threadpoolctl import ThreadpoolController
+
+            _CTL.append(ThreadpoolController())
+        except Exception:  # noqa: BLE001 -- optional: plain numpy without it
+            _CTL.append(None)
+    return _CTL[0]
+
+
 def _start_vector(cfg: BidiagConfig, m: int):
     # bidiag.py:126-131: q = mean + std * N(0,1) from the GK_START stream
     rng = substream(cfg.seed, GK_START)
     q = cfg.start_mean + cfg.start_std * rng.standard_normal(m)
-    beta1 = float(np.linalg.norm(q))
+    beta1 = _host_norm(q)
     if beta1 == 0.0:
         raise NumericalError("start vector has zero norm")
     q /= beta1
@@ -174,7 +203,7 @@ def _terminal_column(lib, h, op: DeviceMatrix, beta: float, rng) -> None:
             if acc.value:
                 return
         v = rng.standard_normal(m)
-        nrm = float(np.linalg.norm(v))
+        nrm = _host_norm(v)
         v_local = np.ascontiguousarray(v[op.row0:op.row0 + op.m_local])
     raise NumericalError("could not extend the left basis to k'+1 columns")
 

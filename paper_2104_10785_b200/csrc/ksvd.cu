@@ -1572,13 +1572,19 @@ struct KlrmHeader {
 };
 static_assert(sizeof(KlrmHeader) == 24, "KLRM header is <4sIQQ");
 
-static int64_t io_chunk_bytes() {
-  static const int64_t v = [] {
+// Staging chunk: 64 MB for file reads and device->host copies; 16 MB for
+// host->device uploads of pageable memory, where the first chunk's copy is
+// not overlapped and a smaller chunk keeps the copy engine fed (measured on
+// the B200 box, tools/r02_upload_chunks.sh: 0.8 GB 34.7 -> 46.6 GB/s, 8 GB
+// 27.6-37 -> 44-49 GB/s; downloads stay faster with 64 MB).
+// KSVD_IO_CHUNK_BYTES overrides both.
+static int64_t io_chunk_bytes(bool upload = false) {
+  static const long long env = [] {
     const char* e = getenv("KSVD_IO_CHUNK_BYTES");
-    const long long b = e ? atoll(e) : (64ll << 20);
-    return (int64_t)std::max(4096ll, b);
+    return e ? atoll(e) : 0ll;
   }();
-  return v;
+  const long long b = env > 0 ? env : (upload ? (16ll << 20) : (64ll << 20));
+  return (int64_t)std::max(4096ll, b);
 }
 
 static bool pread_all(int fd, void* buf, size_t bytes, off_t off) {
@@ -2244,7 +2250,7 @@ static int staged_copy(ksvd_ctx* c, void* dev, size_t dpitch, void* host, size_t
     CK(cudaStreamSynchronize(s));
     return 0;
   }
-  const size_t chunk = std::max<size_t>((size_t)io_chunk_bytes(), width);
+  const size_t chunk = std::max<size_t>((size_t)io_chunk_bytes(to_device), width);
   const int64_t rpc = (int64_t)(chunk / width);
   TRY(ensure_stage(c, (size_t)rpc * width));
   char* d = static_cast<char*>(dev);
@@ -2263,18 +2269,26 @@ static int staged_copy(ksvd_ctx* c, void* dev, size_t dpitch, void* host, size_t
     pend_r = -1;
     return true;
   };
+  static const bool dbg = getenv("KSVD_DEBUG_IO") != nullptr;
+  using clk = std::chrono::steady_clock;
+  double t_wait = 0, t_copy = 0;
+  const auto t_start = clk::now();
   int k = 0;
   for (int64_t r = 0; r < rows; r += rpc, ++k) {
     const int b = k & 1;
     const int64_t nr = std::min(rpc, rows - r);
     char* pk = static_cast<char*>(c->stage[b]);
     if (to_device) {
+      auto t0 = clk::now();
       if (k >= 2) CK(cudaEventSynchronize(c->stage_ev[b]));  // chunk b's DMA is done
+      auto t1 = clk::now();
       char* u = h + (size_t)r * hpitch;
       io_parallel((size_t)nr * width, [&](size_t lo, size_t len) {
         copy_packed(pk, u, hpitch, width, lo, len, true);
         return true;
       });
+      t_wait += std::chrono::duration<double, std::milli>(t1 - t0).count();
+      t_copy += std::chrono::duration<double, std::milli>(clk::now() - t1).count();
       CK(cudaMemcpy2DAsync(d + (size_t)r * dpitch, dpitch, pk, width, width, (size_t)nr,
                            cudaMemcpyHostToDevice, s));
       CK(cudaEventRecord(c->stage_ev[b], s));
@@ -2290,6 +2304,11 @@ static int staged_copy(ksvd_ctx* c, void* dev, size_t dpitch, void* host, size_t
   }
   if (!drain()) return set_err(KSVD_ERUNTIME, "staged download failed");
   CK(cudaStreamSynchronize(s));
+  if (dbg && to_device)
+    fprintf(stderr, "[ksvd] staged upload %.1f MB in %d chunks: %.2f ms (host copies %.2f ms, "
+            "DMA waits %.2f ms)\n", (double)width * rows / 1e6, k,
+            std::chrono::duration<double, std::milli>(clk::now() - t_start).count(), t_copy,
+            t_wait);
   return 0;
 }
 
