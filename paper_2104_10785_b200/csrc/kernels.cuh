@@ -175,6 +175,12 @@ struct AVec<double> {
         : "=d"(v[0]), "=d"(v[1])
         : "l"(p));
   }
+  // with an L2 cache policy (a_policy)
+  __device__ __forceinline__ void load(const double* p, uint64_t pol) {
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::256B.v2.f64 {%0,%1}, [%2], %3;"
+        : "=d"(v[0]), "=d"(v[1])
+        : "l"(p), "l"(pol));
+  }
   __device__ __forceinline__ double get(int k) const { return v[k]; }
 };
 template <>
@@ -186,8 +192,26 @@ struct AVec<float> {
         : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
         : "l"(p));
   }
+  __device__ __forceinline__ void load(const float* p, uint64_t pol) {
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+        : "l"(p), "l"(pol));
+  }
   __device__ __forceinline__ double get(int k) const { return (double)v[k]; }
 };
+
+// L2 policy of the A-streaming loads (k_gemv_n, k_gemv_t2): evict_first
+// (ef) keeps A's lines from displacing the small, reused data (basis tiles,
+// partial sums); ksvd.cu chooses it for A far larger than L2, where the
+// hand-over of A's last rows from one pass to the next is negligible.
+__device__ __forceinline__ uint64_t a_policy(int ef) {
+  uint64_t pol;
+  if (ef)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 
 __device__ __forceinline__ void flag_nonfinite(DevState* st, double v, int step) {
   if (!isfinite(v)) st->nonfinite = 1;  // same value from every writer
@@ -249,7 +273,7 @@ __global__ void __launch_bounds__(kThreads)
 k_gemv_n(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nchunks,
           int ngroups, int64_t nseg, const double* __restrict__ p_src,
           const double* __restrict__ p_scale, double* __restrict__ p_dst, int64_t n_true,
-          double* __restrict__ part, const DevState* st, GemvNFin fin) {
+          double* __restrict__ part, const DevState* st, GemvNFin fin, int a_ef) {
   pdl_wait();
   pdl_trigger(1);
   if (halted(st)) return;
@@ -280,6 +304,7 @@ k_gemv_n(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nch
     }
   }
   const TA* base = A + ((int64_t)chunk * CW + lane) * V;
+  const uint64_t pol = a_policy(a_ef);
   int par = 0;
   const int64_t niter = rseg * 8 < m ? (m - rseg * 8 + nseg * 8 - 1) / (nseg * 8) : 0;
   int64_t it = 0;
@@ -290,7 +315,7 @@ k_gemv_n(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec, int nch
       const int64_t row = min(r + rr, m - 1);  // clamp: duplicate rows are discarded
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (live[u]) a[rr][u].load(base + row * lda + u * 32 * V);
+        if (live[u]) a[rr][u].load(base + row * lda + u * 32 * V, pol);
     }
     double v[8];
 #pragma unroll
@@ -507,7 +532,7 @@ __device__ __forceinline__ void gemv_t2_body(const TA* __restrict__ A, int64_t l
                                              double* __restrict__ part, int64_t ldz,
                                              int64_t bx, int64_t sp, int64_t nsplit,
                                              double* __restrict__ q_s,
-                                             double* __restrict__ red_flat) {
+                                             double* __restrict__ red_flat, int a_ef) {
   constexpr int V = AVec<TA>::V;
   constexpr int TPG = kThreads / RG;
   constexpr int RBT = RG * U * IT;
@@ -521,6 +546,7 @@ __device__ __forceinline__ void gemv_t2_body(const TA* __restrict__ A, int64_t l
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.0;
   const TA* base = A + vcol * V;
+  const uint64_t pol = a_policy(a_ef);
   const int64_t last = sp < nblk ? sp + ((nblk - 1 - sp) / nsplit) * nsplit : -1;
   for (int64_t b = last; b >= 0; b -= nsplit) {
     const int64_t rb = b * RBT;
@@ -541,7 +567,7 @@ __device__ __forceinline__ void gemv_t2_body(const TA* __restrict__ A, int64_t l
     for (; r + (U - 1) * RG < nr; r += U * RG) {
       AVec<TA> a[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) a[u].load(p + (int64_t)(r + u * RG) * lda);
+      for (int u = 0; u < U; ++u) a[u].load(p + (int64_t)(r + u * RG) * lda, pol);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const double qv = q_s[r + u * RG];
@@ -551,7 +577,7 @@ __device__ __forceinline__ void gemv_t2_body(const TA* __restrict__ A, int64_t l
     }
     for (; r < nr; r += RG) {
       AVec<TA> a;
-      a.load(p + (int64_t)r * lda);
+      a.load(p + (int64_t)r * lda, pol);
       const double qv = q_s[r];
 #pragma unroll
       for (int k = 0; k < V; ++k) acc[k] = fma(a.get(k), qv, acc[k]);
@@ -584,7 +610,7 @@ __global__ void __launch_bounds__(kThreads)
 k_gemv_t2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
           int64_t /*unused*/, const double* __restrict__ q_src,
           const double* __restrict__ q_scale, double* __restrict__ q_dst,
-          double* __restrict__ part, int64_t ldz, const DevState* st) {
+          double* __restrict__ part, int64_t ldz, const DevState* st, int a_ef) {
   pdl_wait();
   pdl_trigger(1);
   if (halted(st)) return;
@@ -592,7 +618,7 @@ k_gemv_t2(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t nvec,
   __shared__ double q_s[SM::QS];
   __shared__ double red[SM::RED];
   gemv_t2_body<TA, U, RG, IT>(A, lda, m, nvec, q_src, q_scale, q_dst, part, ldz, blockIdx.x,
-                              blockIdx.y, gridDim.y, q_s, red);
+                              blockIdx.y, gridDim.y, q_s, red, a_ef);
 }
 
 // z[j] = sum_s part[s][j] (- beta p[j]); zero in the padding [n, n_pad).

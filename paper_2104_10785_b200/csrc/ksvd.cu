@@ -414,6 +414,20 @@ static int free_matrix(ksvd_mat* M) {
 // w = A p (- alpha q): partial row sums per chunk group (k_gemv_n), then
 // the group sums + epilogue (k_gemv_n_finalize) unless the caller fuses the
 // finalisation into its k_cgs2_* launch (finalize = false).
+// L2 evict_first for A's loads (kernels.cuh a_policy) when A exceeds 2 GB
+// (16 L2 capacities): same box, configs 3 / 4: k_gemv_n +1.3 / +0.6 %,
+// k_gemv_t2 +0.5 / +0.7 %; on config 2 (0.8 GB) it costs k_gemv_t2 2.5 % of
+// the rows k_gemv_n leaves in L2 (profiles/r02/a_evict_first_ab.txt).
+// KSVD_A_EVICT_FIRST=0/1 forces it.
+static int a_evict_first(const ksvd_mat* M) {
+  static const int force = [] {
+    const char* e = getenv("KSVD_A_EVICT_FIRST");
+    return e ? (strcmp(e, "1") == 0 ? 1 : 0) : -1;
+  }();
+  if (force >= 0) return force;
+  return (size_t)M->mloc * M->lda * esize(M->dtype) >= ((size_t)2 << 30) ? 1 : 0;
+}
+
 // tail_fin (the paired step): the finalisation runs in k_gemv_n's tail
 // (FIN instantiation, per-segment arrival counters M->seg_cnt) instead.
 static int dense_gemv_n(ksvd_mat* M, const double* p_src, const double* p_scale,
@@ -435,7 +449,7 @@ static int dense_gemv_n(ksvd_mat* M, const double* p_src, const double* p_scale,
 #define KSVD_GN(TA, F, B)                                                                   \
   launch_step(c, KC_GEMV_N, k_gemv_n<TA, kUnrollN, F, B>, grid, dim3(kThreads), 0,           \
               (const TA*)M->A, M->lda, M->mloc, pn.nvec, pn.nchunks, pn.ngroups, pn.nseg,    \
-              p_src, p_scale, p_dst, M->n, M->part_n, (const DevState*)st, nf)
+              p_src, p_scale, p_dst, M->n, M->part_n, (const DevState*)st, nf, a_evict_first(M))
   if (M->dtype == KSVD_F32) {
     if (nb) TRY(tail_fin ? KSVD_GN(float, true, true) : KSVD_GN(float, false, true));
     else TRY(tail_fin ? KSVD_GN(float, true, false) : KSVD_GN(float, false, false));
@@ -465,10 +479,10 @@ static int launch_gemv_t(ksvd_mat* M, dim3 grid, const double* q_src, const doub
     if (abytes < ((size_t)2 << 30))
       return launch_step(c, KC_GEMV_T, k_gemv_t2<TA, kUnrollT, 8, 2>, grid, dim3(kThreads), 0,
                     (const TA*)M->A, M->lda, M->mloc, M->pn.nvec, pt.rows_per_split, q_src,
-                    q_scale, q_dst, M->part_t, M->n_pad, (const DevState*)st);
+                    q_scale, q_dst, M->part_t, M->n_pad, (const DevState*)st, a_evict_first(M));
     return launch_step(c, KC_GEMV_T, k_gemv_t2<TA, kUnrollT, 8, 8>, grid, dim3(kThreads), 0,
                   (const TA*)M->A, M->lda, M->mloc, M->pn.nvec, pt.rows_per_split, q_src,
-                  q_scale, q_dst, M->part_t, M->n_pad, (const DevState*)st);
+                  q_scale, q_dst, M->part_t, M->n_pad, (const DevState*)st, a_evict_first(M));
   }
 #define KSVD_GT(RG)                                                                    \
   launch_step(c, KC_GEMV_T, k_gemv_t<TA, kUnrollT, RG>, grid, dim3(kThreads), 0,             \

@@ -30,7 +30,7 @@ float time_n(const TA* A, int64_t lda, int64_t m, int64_t n, const double* p, do
   for (int r = 0; r < 10; ++r) {
     cudaEventRecord(a);
     k<<<(unsigned)blocks, 256>>>(A, lda, m, nvec, nchunks, ngroups, nseg, p, nullptr, nullptr, n,
-                                 part, st, GemvNFin{});
+                                 part, st, GemvNFin{}, 0);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms;
@@ -58,7 +58,7 @@ float timet2(const TA* A, int64_t lda, int64_t m, int64_t n, const double* q, do
   for (int r = 0; r < 10; ++r) {
     cudaEventRecord(a);
     k_gemv_t2<TA, U, RG, IT><<<dim3(tiles, nsplit), 256>>>(A, lda, m, nvec, 0, q, nullptr, nullptr,
-                                                          part, ldz, st);
+                                                          part, ldz, st, 0);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms;

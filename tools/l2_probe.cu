@@ -51,7 +51,7 @@ int main() {
   };
   auto gtk = [&] {
     k_gemv_t2<double, 16, 8, 2><<<gt, 256>>>(A, lda, m, nvec, 0, q, nullptr, nullptr, partt, n,
-                                             st);
+                                             st, 0);
   };
   auto fl = [&] { k_flush<<<1184, 256>>>(flush, kFlushN); };
   auto timed = [&](auto&& f) {
