@@ -128,7 +128,8 @@ def test_nan_and_inf_raise_numerical_error():
 
 def test_golden_and_edges_through_streaming_kernels():
     """The reference-generated golden cases (breakdowns, degenerate and
-    terminal columns included) and this module's edge cases with the
+    terminal columns included), this module's edge cases and the restart
+    suite with the
     whole-loop resident kernel disabled (KSVD_RESIDENT=0): the small shapes
     then run the streaming kernels -- the paired step (k_cgs2_pair, pair.cuh)
     wherever its tiles fit -- in a subprocess (the switch is read once)."""
@@ -148,6 +149,12 @@ def test_golden_and_edges_through_streaming_kernels():
                                      "test_large_eps_breaks_down_immediately",
                                      "test_rank_shapes_and_modes", "test_float32_inputs_everywhere",
                                      "test_nan_and_inf_raise_numerical_error")]
+    rst = root / "tests" / "test_gpu_restart.py"  # thick restarts resume through the paired step
+    ids += [f"{rst}::{t}" for t in ("test_restarted_matches_oracle_and_dense_svd",
+                                    "test_restart_beats_plain_fsvd_at_equal_basis_size",
+                                    "test_restarted_low_rank_f32_and_factored",
+                                    "test_restarted_full_basis_and_errors",
+                                    "test_breakdown_residual_reported_not_zeroed")]
     res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
                           *ids], cwd=root, env={**os.environ, "KSVD_RESIDENT": "0"},
                          capture_output=True, text=True, timeout=1200)
