@@ -2264,7 +2264,12 @@ static int staged_copy(ksvd_ctx* c, void* dev, size_t dpitch, void* host, size_t
     CK(cudaStreamSynchronize(s));
     return 0;
   }
-  const size_t chunk = std::max<size_t>((size_t)io_chunk_bytes(to_device), width);
+  // uploads of a few chunks' worth: at least 8 chunks (>= 2 MB) so that the
+  // copy engine starts early -- 16 MB (config 1) in ~1.0 instead of ~1.6 ms
+  size_t cb = (size_t)io_chunk_bytes(to_device);
+  if (to_device && !getenv("KSVD_IO_CHUNK_BYTES"))
+    cb = std::min(cb, std::max<size_t>((size_t)2 << 20, (width * (size_t)rows + 7) / 8));
+  const size_t chunk = std::max<size_t>(cb, width);
   const int64_t rpc = (int64_t)(chunk / width);
   TRY(ensure_stage(c, (size_t)rpc * width));
   char* d = static_cast<char*>(dev);
